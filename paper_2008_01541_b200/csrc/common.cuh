@@ -1,0 +1,77 @@
+// Shared device-side definitions (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <math_constants.h>
+
+#include "spb_internal.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "schurpd_b200 is built for sm_100a only"
+#endif
+
+namespace spb {
+
+constexpr int NUM_SMS_B200 = 148;
+
+#define SPB_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      spb::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " +    \
+                     __FILE__ + ":" + std::to_string(__LINE__) + " (" #call ")");       \
+      return SPB_ERR_CUDA;                                                              \
+    }                                                                                   \
+  } while (0)
+
+// ------------------------------------------------------------ collider data
+struct ShapeDev {
+  int kind;
+  double p[7];
+  int dims[3];
+  const double* values;  // device, indexed [ix + nx*(iy + ny*iz)]
+};
+
+struct PosedDev {
+  int shape;
+  double R[9];
+  double t[3];
+};
+
+constexpr int MAX_COLLIDERS = 32;
+
+struct ColliderSet {
+  int n;
+  PosedDev posed[MAX_COLLIDERS];
+};
+
+// ------------------------------------------------------------ element data
+struct ElemParams {
+  double mu, mu_prime, smin, smax;
+  int biphasic;
+};
+
+// ------------------------------------------------------------ small utils
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace spb

@@ -1,0 +1,721 @@
+// Scene context + C ABI: device residency of the constant system, the
+// per-frame schedule of solve_frame_schur (reference solver.py:387-455) as a
+// static kernel sequence (captured once per (outer, inner, cadence) as a CUDA
+// graph), state up/download, and the one-shot ops behind the public helpers.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spb {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ------------------------------------------------------------ device buffer
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    free();
+    n = count;
+    if (cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)) != cudaSuccess) {
+      p = nullptr;
+      set_error("cudaMalloc failed (" + std::to_string(sizeof(T) * count) + " bytes)");
+      return SPB_ERR_CUDA;
+    }
+    return SPB_OK;
+  }
+  int upload(const T* h, size_t count) {
+    int rc = alloc(count);
+    if (rc) return rc;
+    if (count && h) SPB_CUDA(cudaMemcpy(p, h, sizeof(T) * count, cudaMemcpyHostToDevice));
+    return SPB_OK;
+  }
+  int upload(const std::vector<T>& v) { return upload(v.data(), v.size()); }
+  int zeros(size_t count) {
+    int rc = alloc(count);
+    if (rc) return rc;
+    SPB_CUDA(cudaMemset(p, 0, sizeof(T) * std::max<size_t>(count, 1)));
+    return SPB_OK;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
+#define TRY(x)                 \
+  do {                         \
+    int _rc = (x);             \
+    if (_rc != SPB_OK) return _rc; \
+  } while (0)
+
+// CSR of (key -> packed source) with sources appended in the given order.
+struct Csr {
+  std::vector<int> ptr, src;
+};
+static Csr make_csr(int nkeys, const std::vector<std::pair<int, int>>& pairs /* (key, src) in order */) {
+  Csr c;
+  c.ptr.assign(nkeys + 1, 0);
+  for (auto& kv : pairs) c.ptr[kv.first + 1]++;
+  for (int k = 0; k < nkeys; ++k) c.ptr[k + 1] += c.ptr[k];
+  c.src.resize(pairs.size());
+  std::vector<int> fill(c.ptr.begin(), c.ptr.end() - 1);
+  for (auto& kv : pairs) c.src[fill[kv.first]++] = kv.second;
+  return c;
+}
+
+// slot-major, element-order node gather of element forces (np.add.at order,
+// material.py:354-356): for slot a, for list position i: node tets[e_i][a]
+static Csr element_gather(const std::vector<int64_t>& tets, const int64_t* sub, int64_t nsub,
+                          const std::vector<int>& node_to_key, int nkeys) {
+  std::vector<std::pair<int, int>> pairs;
+  pairs.reserve(4 * nsub);
+  for (int a = 0; a < 4; ++a)
+    for (int64_t i = 0; i < nsub; ++i) {
+      int64_t e = sub ? sub[i] : i;
+      int key = node_to_key[tets[4 * e + a]];
+      if (key >= 0) pairs.emplace_back(key, (int)(i * 4 + a));
+    }
+  return make_csr(nkeys, pairs);
+}
+
+static void to_soa9(const double* aos, int64_t ne, std::vector<double>& soa) {
+  soa.resize(9 * ne);
+  for (int64_t e = 0; e < ne; ++e)
+    for (int c = 0; c < 9; ++c) soa[c * ne + e] = aos[9 * e + c];
+}
+
+// --------------------------------------------------------------- context
+struct Ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int64_t n = 0, ne = 0;
+  int n1 = 0, n2 = 0, na = 0, nalpha = 0, nbeta = 0, P = 0;
+  ElemParams ep{};
+  Factor* factor = nullptr;
+
+  DBuf<int4> tets;
+  DBuf<double> dmi, vol, x, R, Q;
+  DBuf<int> e_alpha, e_beta;
+  DBuf<double> Ga, Gb;
+  DBuf<int> ga_ptr, ga_src, fac_node, att_ptr, att_idx, att_nodes;
+  DBuf<double> att_k, att_tgt;
+  DBuf<double> b, y, U, XF;
+  DBuf<int> gb_ptr, gb_src, gc_ptr, gc_src;
+  DBuf<int> prox_elem, prox_local;
+  DBuf<double> prox_w, prox_c, vprox, target;
+  DBuf<uint8_t> active;
+  DBuf<int> x2_ids, x1_node;
+  DBuf<double> f_tilde2, u2acc, g, u2, s0u;
+  DBuf<int> k_ptr, k_idx;
+  DBuf<double> k_val;
+  // dense
+  int N = 0, ntasks = 0;
+  DBuf<double> sigma0_tiles, L, Linv, Y, gemv_partial, xrows;
+  DBuf<int> flags, counter, info, xflags;
+  DBuf<int2> tasks;
+  DBuf<int> c22_tile_ptr, c22_ent_rc, c22_ent_ptr, c22_contrib;
+  DenseDev dd{};
+  // colliders
+  std::vector<ShapeDev> shapes;
+  std::vector<double*> shape_vals;
+  DBuf<ShapeDev> shapes_dev;
+  bool shapes_dirty = true;
+  ColliderSet* cols_host = nullptr;  // pinned
+  DBuf<ColliderSet> cols_dev;
+  double* att_tgt_host = nullptr;    // pinned staging
+  // metrics
+  DBuf<double> e_part, a_part, p_part, r_part, metrics_out;
+  double* metrics_host = nullptr;    // pinned
+  int e_blocks = 0, a_blocks = 0, p_blocks = 0, r_blocks = 0;
+  // early-exit (lazily built)
+  bool have_all_gather = false;
+  DBuf<double> Gall, fall;
+  DBuf<int> gall_ptr, gall_src, att_ptr_node, att_idx_node, node_ids;
+  // graph cache
+  std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+  int last_launches = 0;
+  bool residual_valid = false;
+
+  ProxyDev px() const { return ProxyDev{P, prox_elem.p, prox_w.p, prox_c.p, prox_local.p}; }
+
+  ~Ctx() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (double* v : shape_vals) cudaFree(v);
+    if (cols_host) cudaFreeHost(cols_host);
+    if (att_tgt_host) cudaFreeHost(att_tgt_host);
+    if (metrics_host) cudaFreeHost(metrics_host);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  int create(const spb_scene_desc* s, Factor* f, int dev);
+  int enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev /* 7 phase events or null */);
+  int sync_shapes();
+};
+
+int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
+  device = dev;
+  SPB_CUDA(cudaSetDevice(device));
+  SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  factor = f;
+  n = s->num_nodes;
+  ne = s->num_elements;
+  n1 = (int)s->n1;
+  n2 = (int)s->n2;
+  na = (int)s->num_attachments;
+  nalpha = (int)s->num_alpha;
+  nbeta = (int)s->num_beta;
+  P = (int)s->num_proxies;
+  if (n1 + n2 != n || f->n1 != n1 || f->n2 != n2) { set_error("scene/factor sizes disagree"); return SPB_ERR_ARG; }
+  if (n >= (1LL << 31) / 3 || ne >= (1LL << 31)) { set_error("mesh too large for 32-bit ids"); return SPB_ERR_ARG; }
+  ep = ElemParams{s->mu, s->mu_prime, s->sigma_min, s->sigma_max, s->mu_prime > 0.0 ? 1 : 0};
+
+  std::vector<int64_t> tets_h(s->tets, s->tets + 4 * ne);
+  std::vector<int4> t4(ne);
+  for (int64_t e = 0; e < ne; ++e)
+    t4[e] = make_int4((int)tets_h[4 * e], (int)tets_h[4 * e + 1], (int)tets_h[4 * e + 2], (int)tets_h[4 * e + 3]);
+  TRY(tets.upload(t4));
+  std::vector<double> soa;
+  to_soa9(s->dm_inverse, ne, soa);
+  TRY(dmi.upload(soa));
+  TRY(vol.upload(s->volume, ne));
+  TRY(x.zeros(3 * n));
+  // R = I (RotationCache.identity, material.py:60-63)
+  std::vector<double> eye(9 * ne, 0.0);
+  for (int64_t e = 0; e < ne; ++e) eye[0 * ne + e] = eye[4 * ne + e] = eye[8 * ne + e] = 1.0;
+  TRY(R.upload(eye));
+  if (ep.biphasic) TRY(Q.upload(eye));
+  std::vector<int> ea(s->e_alpha, s->e_alpha + nalpha), eb(s->e_beta, s->e_beta + nbeta);
+  TRY(e_alpha.upload(ea));
+  TRY(e_beta.upload(eb));
+  TRY(Ga.alloc(12 * (size_t)std::max(nalpha, 1)));
+  TRY(Gb.alloc(12 * (size_t)std::max(nbeta, 1)));
+
+  // factor-order node map: rows [0,n1) = x1 in fill order, [n1,n) = x2
+  std::vector<int64_t> order(n);
+  for (int64_t i = 0; i < n; ++i) order[s->perm[i]] = i;  // order[new] = old
+  std::vector<int> fac(n), key_of_node(n);
+  for (int k = 0; k < n1; ++k) fac[k] = (int)order[f->fill_perm[k]];
+  for (int k = 0; k < n2; ++k) fac[n1 + k] = (int)order[n1 + k];
+  for (int k = 0; k < n; ++k) key_of_node[fac[k]] = k;
+  TRY(fac_node.upload(fac));
+  std::vector<int> x1n(fac.begin(), fac.begin() + n1), x2n(fac.begin() + n1, fac.end());
+  TRY(x1_node.upload(x1n));
+  TRY(x2_ids.upload(x2n));
+  // alpha gather in factor order + attachments in list order
+  Csr ga = element_gather(tets_h, s->e_alpha, nalpha, key_of_node, (int)n);
+  TRY(ga_ptr.upload(ga.ptr));
+  TRY(ga_src.upload(ga.src));
+  std::vector<std::pair<int, int>> ap;
+  for (int a = 0; a < na; ++a) ap.emplace_back(key_of_node[s->att_nodes[a]], a);
+  Csr ac = make_csr((int)n, ap);
+  TRY(att_ptr.upload(ac.ptr));
+  TRY(att_idx.upload(ac.src));
+  TRY(att_k.upload(s->att_stiffness, na));
+  std::vector<int> an(na);
+  for (int a = 0; a < na; ++a) an[a] = (int)s->att_nodes[a];
+  TRY(att_nodes.upload(an));
+  TRY(att_tgt.zeros(3 * (size_t)na));
+  SPB_CUDA(cudaMallocHost(&att_tgt_host, sizeof(double) * 3 * std::max(na, 1)));
+  TRY(b.zeros(3 * (size_t)n));
+  TRY(y.zeros(3 * (size_t)std::max(n1, 1)));
+  TRY(XF.zeros(3 * (size_t)n));
+  if (n1 > 0) {
+    TRY(build_device_factor(*f));
+    TRY(U.zeros(3 * std::max<size_t>(device_factor_ubuf(*f->dev), 1)));
+  }
+  // beta gather (trailing-local keys) and proxies
+  std::vector<int> key2(n, -1);
+  for (int k = 0; k < n2; ++k) key2[fac[n1 + k]] = k;
+  Csr gb = element_gather(tets_h, s->e_beta, nbeta, key2, n2);
+  TRY(gb_ptr.upload(gb.ptr));
+  TRY(gb_src.upload(gb.src));
+  std::vector<int> pe(P), pl(4 * (size_t)P);
+  std::vector<std::pair<int, int>> cp;
+  for (int j = 0; j < P; ++j) {
+    int64_t e = s->proxy_elements[j];
+    pe[j] = (int)e;
+    for (int a = 0; a < 4; ++a) {
+      int64_t node = tets_h[4 * e + a];
+      int l = (int)(s->perm[node] - n1);
+      if (l < 0) {
+        set_error("proxy " + std::to_string(j) + " touches a node outside the collision-prone range");
+        return SPB_ERR_PARTITION;
+      }
+      pl[4 * j + a] = l;
+    }
+  }
+  for (int a = 0; a < 4; ++a)  // (slot, proxy) order: solver.py:362-363
+    for (int j = 0; j < P; ++j) cp.emplace_back(pl[4 * j + a], j * 4 + a);
+  Csr gc = make_csr(n2, cp);
+  TRY(gc_ptr.upload(gc.ptr));
+  TRY(gc_src.upload(gc.src));
+  TRY(prox_elem.upload(pe));
+  TRY(prox_local.upload(pl));
+  TRY(prox_w.upload(s->proxy_weights, 4 * (size_t)P));
+  TRY(prox_c.upload(s->proxy_stiffness, P));
+  TRY(active.zeros(std::max(P, 1)));
+  TRY(target.zeros(3 * (size_t)std::max(P, 1)));
+  TRY(vprox.zeros(3 * (size_t)std::max(P, 1)));
+  TRY(f_tilde2.zeros(3 * (size_t)std::max(n2, 1)));
+  TRY(u2acc.zeros(3 * (size_t)std::max(n2, 1)));
+  TRY(g.zeros(3 * (size_t)std::max(n2, 1)));
+  TRY(u2.zeros(3 * (size_t)std::max(n2, 1)));
+  TRY(s0u.zeros(3 * (size_t)std::max(n2, 1)));
+  // K22_beta CSR
+  if (n2 > 0) {
+    int64_t nnz = s->k22_indptr[n2];
+    std::vector<int> kp(n2 + 1), ki(nnz);
+    for (int k = 0; k <= n2; ++k) kp[k] = (int)s->k22_indptr[k];
+    for (int64_t q = 0; q < nnz; ++q) ki[q] = (int)s->k22_indices[q];
+    TRY(k_ptr.upload(kp));
+    TRY(k_idx.upload(ki));
+    TRY(k_val.upload(s->k22_data, nnz));
+  }
+
+  // ---- dense: sigma0 tiles (lower, padded with identity), C22 by tile
+  if (n2 > 0) {
+    N = (n2 + 63) / 64;
+    const int nt = dense_tile_count(N);
+    std::vector<double> tiles((size_t)nt * 4096, 0.0);
+    for (int i = 0; i < N; ++i)
+      for (int j = 0; j <= i; ++j) {
+        double* T = tiles.data() + (size_t)(i * (i + 1) / 2 + j) * 4096;
+        for (int r = 0; r < 64; ++r)
+          for (int c = 0; c < 64; ++c) {
+            int gr = i * 64 + r, gcc = j * 64 + c;
+            double v = 0.0;
+            if (gr < n2 && gcc < n2) v = f->sigma0[(size_t)gr * n2 + gcc];
+            else if (gr == gcc) v = 1.0;
+            T[r * 64 + c] = v;
+          }
+      }
+    TRY(sigma0_tiles.upload(tiles));
+    TRY(L.zeros((size_t)nt * 4096));
+    TRY(Linv.zeros((size_t)N * 4096));
+    TRY(Y.zeros((size_t)N * 4096));
+    TRY(flags.zeros(nt + N));
+    TRY(counter.zeros(1));
+    TRY(info.zeros(1));
+    TRY(xflags.zeros(N));
+    TRY(xrows.zeros((size_t)N * 3 * 64));
+    TRY(gemv_partial.zeros((size_t)nt * 6 * 64));
+    std::vector<int2> tk;
+    for (int j = 0; j < N; ++j) {
+      for (int i = j; i < N; ++i) tk.push_back(make_int2(i, j));
+      tk.push_back(make_int2(N, j));
+    }
+    ntasks = (int)tk.size();
+    TRY(tasks.upload(tk));
+    // C22 entries: upper (c, r) COO contributions in (proxy, a, b) order, stored at
+    // lower (r, c) (linalg.py:46-51, :67-74 + collision.py:431-434)
+    std::map<std::pair<int, int>, std::vector<int>> ent;  // (tile, rc) -> codes
+    for (int j = 0; j < P; ++j)
+      for (int a = 0; a < 4; ++a)
+        for (int bb = 0; bb < 4; ++bb) {
+          int ra = pl[4 * j + a], cb = pl[4 * j + bb];
+          if (ra > cb) continue;  // upper entry (row ra <= col cb) -> lower (cb, ra)
+          int gr = cb, gcc = ra;
+          int ti = gr / 64, tj = gcc / 64;
+          int t = ti * (ti + 1) / 2 + tj;
+          int rc = (gr % 64) * 64 + (gcc % 64);
+          ent[{t, rc}].push_back(j * 16 + a * 4 + bb);
+        }
+    std::vector<int> tptr(nt + 1, 0), erc, eptr(1, 0), codes;
+    for (auto& kv : ent) {
+      tptr[kv.first.first + 1]++;
+      erc.push_back(kv.first.second);
+      codes.insert(codes.end(), kv.second.begin(), kv.second.end());
+      eptr.push_back((int)codes.size());
+    }
+    for (int t = 0; t < nt; ++t) tptr[t + 1] += tptr[t];
+    TRY(c22_tile_ptr.upload(tptr));
+    TRY(c22_ent_rc.upload(erc));
+    TRY(c22_ent_ptr.upload(eptr));
+    TRY(c22_contrib.upload(codes));
+    dd = DenseDev{n2, N, sigma0_tiles.p, L.p, Linv.p, Y.p, flags.p, counter.p, info.p,
+                  c22_tile_ptr.p, c22_ent_rc.p, c22_ent_ptr.p, c22_contrib.p, prox_w.p, prox_c.p, active.p};
+  }
+  // colliders + metrics
+  SPB_CUDA(cudaMallocHost(&cols_host, sizeof(ColliderSet)));
+  memset(cols_host, 0, sizeof(ColliderSet));
+  TRY(cols_dev.zeros(1));
+  e_blocks = energy_blocks(ne);
+  a_blocks = attachment_blocks(na);
+  p_blocks = proxy_blocks(P);
+  r_blocks = update_blocks(n2);
+  TRY(e_part.zeros(std::max(e_blocks, 1)));
+  TRY(a_part.zeros(std::max(a_blocks, 1)));
+  TRY(p_part.zeros(2 * (size_t)std::max(p_blocks, 1)));
+  TRY(r_part.zeros(2 * (size_t)std::max(r_blocks, 1)));
+  TRY(metrics_out.zeros(4));
+  SPB_CUDA(cudaMallocHost(&metrics_host, sizeof(double) * 4));
+  SPB_CUDA(cudaDeviceSynchronize());
+  return SPB_OK;
+}
+
+int Ctx::sync_shapes() {
+  if (!shapes_dirty) return SPB_OK;
+  TRY(shapes_dev.upload(shapes.data(), shapes.size()));
+  shapes_dirty = false;
+  return SPB_OK;
+}
+
+// The frame: solve_frame_schur (solver.py:387-455) + _finish_metrics (:373-384).
+// ev (optional): 7 events recorded at phase boundaries of the LAST pass:
+//   0 start, 1 after local+forces, 2 after forward, 3 after inner loop,
+//   4 after backward, 5 after metrics.
+int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
+  int launches = 0;
+  const ProxyDev P_ = px();
+  bool first_detection_done = false;
+  residual_valid = false;
+  if (ev) SPB_CUDA(cudaEventRecord(ev[0], st));
+  for (int o = 0; o < outer; ++o) {
+    // (1) local step on E_alpha fused with (2) the alpha element forces
+    launch_local_forces(st, nalpha, e_alpha.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Ga.p, 1);
+    launch_gather_forces(st, (int)n, ga_ptr.p, ga_src.p, Ga.p, nalpha, fac_node.p, att_ptr.p, att_idx.p, att_k.p,
+                         att_tgt.p, x.p, b.p);
+    launches += (nalpha > 0) + 1;
+    if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[1], st));
+    // (3) forward substitution: y1 = L1^-1 f1[fill], f~2 = f2 - C y1
+    if (n1 > 0) {
+      sparse_forward(st, *factor->dev, b.p, y.p, U.p, f_tilde2.p, &launches);
+    } else if (n2 > 0) {
+      SPB_CUDA(cudaMemcpyAsync(f_tilde2.p, b.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice, st));
+    }
+    if (n2 > 0) SPB_CUDA(cudaMemsetAsync(u2acc.p, 0, sizeof(double) * 3 * n2, st));
+    if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[2], st));
+    for (int it = 0; it < inner; ++it) {
+      bool fresh = cadence == SPB_CADENCE_INNER || (cadence == SPB_CADENCE_FRAME && !first_detection_done);
+      if (fresh && P > 0) {
+        launch_detect(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
+        launches++;
+      }
+      first_detection_done = true;
+      if (n2 == 0) continue;
+      // (4.2) local step on E_beta fused with the beta element forces
+      launch_local_forces(st, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
+      // (4.4) g = f~2 + f_beta + f_col, packed as the RHS tile row
+      launch_build_g(st, n2, f_tilde2.p, gb_ptr.p, gb_src.p, Gb.p, nbeta, P_, tets.p, x.p, active.p, target.p,
+                     gc_ptr.p, gc_src.p, g.p, Y.p);
+      // (4.3)+(4.5) H = sigma0 + C22, LL^T = H, y = L^-1 g (one persistent launch), u2 = L^-T y
+      SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
+      SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
+      SPB_CUDA(cudaMemsetAsync(xflags.p, 0, sizeof(int) * N, st));
+      launch_cholesky_tiles(st, dd, tasks.p, ntasks, NUM_SMS_B200);
+      launch_dense_backward(st, dd, xflags.p, xrows.p, u2.p);
+      // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual
+      launch_sym_tile_gemv(st, dd, u2.p, gemv_partial.p);
+      launch_sym_tile_gemv_reduce(st, dd, gemv_partial.p, s0u.p);
+      launch_proxy_wu(st, P_, active.p, u2.p, vprox.p);
+      launch_inner_update(st, n2, u2.p, s0u.p, k_ptr.p, k_idx.p, k_val.p, g.p, prox_w.p, vprox.p, gc_ptr.p,
+                          gc_src.p, f_tilde2.p, u2acc.p, x.p, x2_ids.p, r_part.p);
+      launches += (nbeta > 0) + 7 + (P > 0);
+      residual_valid = true;
+    }
+    if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[3], st));
+    // (5) u1 = L1^-T (y1 - C^T u2_accum); x1 += u1
+    if (n1 > 0) {
+      if (n2 > 0)
+        SPB_CUDA(cudaMemcpyAsync(XF.p + 3 * (size_t)n1, u2acc.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice,
+                                 st));
+      sparse_backward(st, *factor->dev, y.p, XF.p, &launches);
+      launch_scatter_add(st, n1, x1_node.p, XF.p, x.p);
+      launches++;
+    }
+    if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[4], st));
+  }
+  // metrics: full-mesh energy, max penetration, active count, residual
+  launch_elastic_energy(st, ne, tets.p, x.p, dmi.p, vol.p, R.p, Q.p, ep, e_part.p);
+  launch_attachment_energy(st, na, att_nodes.p, att_k.p, att_tgt.p, x.p, a_part.p);
+  launch_proxy_final(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, p_part.p);
+  launch_finish_metrics(st, e_part.p, e_blocks, a_part.p, a_blocks, p_part.p, p_blocks, r_part.p,
+                        residual_valid ? r_blocks : 0, active.p, P, 1, metrics_out.p);
+  launches += 4;
+  if (ev) SPB_CUDA(cudaEventRecord(ev[5], st));
+  last_launches = launches;
+  return SPB_OK;
+}
+
+}  // namespace spb
+
+using spb::Ctx;
+using spb::Factor;
+
+// ================================================================== C ABI
+extern "C" {
+
+int32_t spb_version(void) { return 100; }
+const char* spb_last_error(void) { return spb::g_last_error.c_str(); }
+int32_t spb_device_count(int32_t* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    *count = 0;
+    spb::set_error(std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    return SPB_ERR_CUDA;
+  }
+  *count = c;
+  return SPB_OK;
+}
+
+int32_t spb_ctx_create(const spb_scene_desc* scene, const spb_factor* factor, int32_t device, spb_ctx** out) {
+  SPB_GUARD_BEGIN
+  if (!scene || !factor || !out) { spb::set_error("null argument"); return SPB_ERR_ARG; }
+  auto* c = new Ctx();
+  int rc = c->create(scene, const_cast<Factor*>(reinterpret_cast<const Factor*>(factor)), device);
+  if (rc != SPB_OK) { delete c; *out = nullptr; return rc; }
+  *out = reinterpret_cast<spb_ctx*>(c);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+void spb_ctx_destroy(spb_ctx* ctx) { delete reinterpret_cast<Ctx*>(ctx); }
+
+int32_t spb_ctx_add_shape(spb_ctx* cp, const spb_shape_desc* d, int32_t* shape_id) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  spb::ShapeDev s{};
+  s.kind = d->kind;
+  for (int k = 0; k < 7; ++k) s.p[k] = d->params[k];
+  s.values = nullptr;
+  if (d->kind == SPB_SHAPE_LEVELSET) {
+    for (int k = 0; k < 3; ++k) s.dims[k] = (int)d->dims[k];
+    size_t cnt = (size_t)d->dims[0] * d->dims[1] * d->dims[2];
+    double* v = nullptr;
+    SPB_CUDA(cudaMalloc(&v, sizeof(double) * cnt));
+    SPB_CUDA(cudaMemcpy(v, d->values, sizeof(double) * cnt, cudaMemcpyHostToDevice));
+    c->shape_vals.push_back(v);
+    s.values = v;
+  }
+  c->shapes.push_back(s);
+  c->shapes_dirty = true;
+  *shape_id = (int32_t)c->shapes.size() - 1;
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_set_pose(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  if (ncol > spb::MAX_COLLIDERS) { spb::set_error("too many colliders"); return SPB_ERR_ARG; }
+  if (c->na > 0 && att_targets) {
+    memcpy(c->att_tgt_host, att_targets, sizeof(double) * 3 * c->na);
+    SPB_CUDA(cudaMemcpyAsync(c->att_tgt.p, c->att_tgt_host, sizeof(double) * 3 * c->na, cudaMemcpyHostToDevice,
+                             c->st));
+  }
+  SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
+  c->cols_host->n = ncol;
+  for (int i = 0; i < ncol; ++i) {
+    if (cols[i].shape < 0 || cols[i].shape >= (int)c->shapes.size()) {
+      spb::set_error("unknown collider shape id");
+      return SPB_ERR_ARG;
+    }
+    c->cols_host->posed[i].shape = cols[i].shape;
+    memcpy(c->cols_host->posed[i].R, cols[i].rotation, sizeof(double) * 9);
+    memcpy(c->cols_host->posed[i].t, cols[i].translation, sizeof(double) * 3);
+  }
+  TRY(c->sync_shapes());
+  SPB_CUDA(cudaMemcpyAsync(c->cols_dev.p, c->cols_host, sizeof(spb::ColliderSet), cudaMemcpyHostToDevice, c->st));
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_set_state(spb_ctx* cp, const double* x, const double* R, const double* Q, const uint8_t* active,
+                          const double* target, const double* f_tilde2, const double* u2_accum) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  if (x) SPB_CUDA(cudaMemcpy(c->x.p, x, sizeof(double) * 3 * c->n, cudaMemcpyHostToDevice));
+  std::vector<double> soa;
+  if (R) {
+    spb::to_soa9(R, c->ne, soa);
+    SPB_CUDA(cudaMemcpy(c->R.p, soa.data(), sizeof(double) * 9 * c->ne, cudaMemcpyHostToDevice));
+  }
+  if (Q && c->ep.biphasic) {
+    spb::to_soa9(Q, c->ne, soa);
+    SPB_CUDA(cudaMemcpy(c->Q.p, soa.data(), sizeof(double) * 9 * c->ne, cudaMemcpyHostToDevice));
+  }
+  if (active && c->P) SPB_CUDA(cudaMemcpy(c->active.p, active, c->P, cudaMemcpyHostToDevice));
+  if (target && c->P) SPB_CUDA(cudaMemcpy(c->target.p, target, sizeof(double) * 3 * c->P, cudaMemcpyHostToDevice));
+  if (f_tilde2 && c->n2)
+    SPB_CUDA(cudaMemcpy(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2, cudaMemcpyHostToDevice));
+  if (u2_accum && c->n2)
+    SPB_CUDA(cudaMemcpy(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2, cudaMemcpyHostToDevice));
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_get_state(spb_ctx* cp, double* x, double* R, double* Q, uint8_t* active, double* target,
+                          double* f_tilde2, double* u2_accum) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  if (x) SPB_CUDA(cudaMemcpy(x, c->x.p, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost));
+  auto soa_down = [&](const double* d, double* h) -> int {
+    std::vector<double> soa(9 * c->ne);
+    SPB_CUDA(cudaMemcpy(soa.data(), d, sizeof(double) * 9 * c->ne, cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < c->ne; ++e)
+      for (int k = 0; k < 9; ++k) h[9 * e + k] = soa[k * c->ne + e];
+    return SPB_OK;
+  };
+  if (R) TRY(soa_down(c->R.p, R));
+  if (Q && c->ep.biphasic) TRY(soa_down(c->Q.p, Q));
+  if (active && c->P) SPB_CUDA(cudaMemcpy(active, c->active.p, c->P, cudaMemcpyDeviceToHost));
+  if (target && c->P) SPB_CUDA(cudaMemcpy(target, c->target.p, sizeof(double) * 3 * c->P, cudaMemcpyDeviceToHost));
+  if (f_tilde2 && c->n2)
+    SPB_CUDA(cudaMemcpy(f_tilde2, c->f_tilde2.p, sizeof(double) * 3 * c->n2, cudaMemcpyDeviceToHost));
+  if (u2_accum && c->n2)
+    SPB_CUDA(cudaMemcpy(u2_accum, c->u2acc.p, sizeof(double) * 3 * c->n2, cudaMemcpyDeviceToHost));
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
+  const int outer = cfg->outer_iters, inner = cfg->inner_iters, cad = cfg->cadence;
+  TRY(c->sync_shapes());
+  if (cfg->use_graph && !ev) {
+    auto key = std::make_tuple(outer, inner, cad);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      cudaGraph_t gph;
+      SPB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+      int rc = c->enqueue_frame(outer, inner, cad, nullptr);
+      cudaError_t e2 = cudaStreamEndCapture(c->st, &gph);
+      if (rc != SPB_OK) return rc;
+      if (e2 != cudaSuccess) { spb::set_error(std::string("graph capture: ") + cudaGetErrorString(e2)); return SPB_ERR_CUDA; }
+      cudaGraphExec_t exe;
+      SPB_CUDA(cudaGraphInstantiate(&exe, gph, 0));
+      cudaGraphDestroy(gph);
+      it = c->graphs.emplace(key, exe).first;
+    }
+    SPB_CUDA(cudaGraphLaunch(it->second, c->st));
+    return SPB_OK;
+  }
+  return c->enqueue_frame(outer, inner, cad, ev);
+}
+
+int32_t spb_ctx_step(spb_ctx* cp, const spb_step_config* cfg, spb_frame_metrics* m) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  if (cfg->outer_iters < 1 || cfg->inner_iters < 1) { spb::set_error("outer_iters and inner_iters must be >= 1"); return SPB_ERR_ARG; }
+  auto t0 = std::chrono::steady_clock::now();
+  memset(m, 0, sizeof(*m));
+  if (c->n2 > 0) SPB_CUDA(cudaMemsetAsync(c->info.p, 0, sizeof(int), c->st));
+  cudaEvent_t ev[6];
+  bool timed = !cfg->use_graph;
+  if (timed)
+    for (auto& e : ev) SPB_CUDA(cudaEventCreate(&e));
+  int rc = run_frame(c, cfg, timed ? ev : nullptr);
+  if (rc != SPB_OK) return rc;
+  SPB_CUDA(cudaMemcpyAsync(c->metrics_host, c->metrics_out.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
+  int info_h = 0;
+  if (c->n2 > 0) SPB_CUDA(cudaMemcpyAsync(&info_h, c->info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  if (timed) {
+    float a;
+    cudaEventElapsedTime(&a, ev[0], ev[1]); m->t_local_ms = a;
+    cudaEventElapsedTime(&a, ev[1], ev[2]); m->t_forward_ms = a;
+    cudaEventElapsedTime(&a, ev[2], ev[3]); m->t_dense_ms = a;
+    cudaEventElapsedTime(&a, ev[3], ev[4]); m->t_backward_ms = a;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  m->energy = c->metrics_host[0];
+  m->max_penetration = c->metrics_host[1];
+  m->residual = c->residual_valid ? c->metrics_host[2] : 0.0;
+  m->active_proxies = (int64_t)llround(c->metrics_host[3]);
+  m->kernel_launches = c->last_launches;
+  m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (info_h > 0) {
+    m->info = info_h - 1;
+    spb::set_error("dense factorization failed: non-positive pivot");
+    return SPB_ERR_INDEFINITE;
+  }
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_bench(spb_ctx* cp, const spb_step_config* cfg, int32_t frames, double* ms_per_frame,
+                      double* phase_ms) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  cudaEvent_t e0, e1;
+  SPB_CUDA(cudaEventCreate(&e0));
+  SPB_CUDA(cudaEventCreate(&e1));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  SPB_CUDA(cudaEventRecord(e0, c->st));
+  for (int f = 0; f < frames; ++f) TRY(run_frame(c, cfg, nullptr));
+  SPB_CUDA(cudaEventRecord(e1, c->st));
+  SPB_CUDA(cudaEventSynchronize(e1));
+  float ms;
+  SPB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_per_frame = ms / std::max(frames, 1);
+  if (phase_ms) {
+    cudaEvent_t ev[6];
+    for (auto& e : ev) SPB_CUDA(cudaEventCreate(&e));
+    TRY(c->enqueue_frame(cfg->outer_iters, cfg->inner_iters, cfg->cadence, ev));
+    SPB_CUDA(cudaStreamSynchronize(c->st));
+    for (int k = 0; k < 5; ++k) {
+      float a = 0;
+      cudaEventElapsedTime(&a, ev[k], ev[k + 1]);
+      phase_ms[k] = a;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  if (c->n2 == 0) { *ms = 0; return SPB_OK; }
+  SPB_CUDA(cudaSetDevice(c->device));
+  cudaEvent_t e0, e1;
+  SPB_CUDA(cudaEventCreate(&e0));
+  SPB_CUDA(cudaEventCreate(&e1));
+  float tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
+    SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
+    SPB_CUDA(cudaEventRecord(e0, c->st));
+    spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, spb::NUM_SMS_B200);
+    SPB_CUDA(cudaEventRecord(e1, c->st));
+    SPB_CUDA(cudaEventSynchronize(e1));
+    float ms1;
+    SPB_CUDA(cudaEventElapsedTime(&ms1, e0, e1));
+    tot += ms1;
+  }
+  SPB_CUDA(cudaGetLastError());
+  *ms = tot / std::max(reps, 1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+}  // extern "C"

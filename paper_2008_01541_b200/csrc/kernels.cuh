@@ -1,0 +1,95 @@
+// Host-side launchers of the device kernels (one translation unit per family).
+#pragma once
+
+#include "common.cuh"
+
+namespace spb {
+
+// ---------------------------------------------------------------- element.cu
+void launch_local_forces(cudaStream_t st, int nsub, const int* sub, const int4* tets, const double* x,
+                         const double* dmi, const double* vol, int64_t ne, double* R, double* Q,
+                         const ElemParams& p, double* G, int project);
+void launch_gather_forces(cudaStream_t st, int nout, const int* ptr, const int* src, const double* G, int nsub,
+                          const int* out_node, const int* aptr, const int* aidx, const double* ak,
+                          const double* atgt, const double* x, double* out);
+int energy_blocks(int64_t ne);
+void launch_elastic_energy(cudaStream_t st, int64_t ne, const int4* tets, const double* x, const double* dmi,
+                           const double* vol, const double* R, const double* Q, const ElemParams& p,
+                           double* partial);
+void launch_deformation_gradients(cudaStream_t st, int nsub, const int* sub, const int4* tets, const double* x,
+                                  const double* dmi, int64_t ne, double* F);
+void launch_svd_op(cudaStream_t st, int64_t k, const double* F, double* U, double* S, double* V, double* R,
+                   double* Q, double smin, double smax);
+
+// -------------------------------------------------------------- collision.cu
+struct ProxyDev {
+  int P;
+  const int* elem;    // (P)
+  const double* w;    // (P,4)
+  const double* c;    // (P)
+  const int* local;   // (P,4) trailing-local node ids (perm - n1)
+};
+void launch_detect(cudaStream_t st, const ProxyDev& px, const int4* tets, const double* x, const ShapeDev* shapes,
+                   const ColliderSet* cols, uint8_t* active, double* target, double* depth);
+void launch_build_g(cudaStream_t st, int m, const double* f_tilde2, const int* bptr, const int* bsrc,
+                    const double* Gb, int nbeta, const ProxyDev& px, const int4* tets, const double* x,
+                    const uint8_t* active, const double* target, const int* cptr, const int* csrc, double* g,
+                    double* ytile);
+int proxy_blocks(int P);
+void launch_proxy_final(cudaStream_t st, const ProxyDev& px, const int4* tets, const double* x,
+                        const ShapeDev* shapes, const ColliderSet* cols, const uint8_t* active,
+                        const double* target, double* partial);
+
+// ------------------------------------------------------------------ dense.cu
+struct DenseDev {
+  int m, N;                  // order and tile count (T = 64)
+  const double* sigma0;      // lower tiles, tile-major (diagonal tiles full)
+  double* L;                 // factor tiles
+  double* Linv;              // inverse diagonal tiles (N)
+  double* Y;                 // RHS tile row (N tiles): rows 0..2 = g^T, then y^T
+  int* flags;                // N(N+1)/2 + N readiness flags
+  int* counter;              // task counter
+  int* info;                 // first failing column + 1 (0 = ok)
+  // C22 by tile: entries (tile-local r*64+c) and their contributions
+  // (proxy j, slot a, slot b) in the reference's COO order
+  const int* c22_tile_ptr;   // (ntiles+1)
+  const int* c22_ent_rc;     // (E)
+  const int* c22_ent_ptr;    // (E+1)
+  const int* c22_contrib;    // (C) j*16 + a*4 + b
+  const double* proxy_w;
+  const double* proxy_c;
+  const uint8_t* active;
+};
+int dense_tile_count(int N);
+size_t cholesky_smem_bytes();
+void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid);
+void launch_dense_backward(cudaStream_t st, const DenseDev& d, int* xflags, double* xrows, double* u);
+void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial);
+void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out);
+
+// ----------------------------------------------------------------- sparse.cu
+struct DeviceFactor;
+int build_device_factor(Factor& f);
+void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
+                    int* launches);
+void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches);
+size_t device_factor_ubuf(const DeviceFactor& df);
+int device_factor_levels(const DeviceFactor& df);
+
+// ----------------------------------------------------------------- update.cu
+void launch_proxy_wu(cudaStream_t st, const ProxyDev& px, const uint8_t* active, const double* u2, double* v);
+int update_blocks(int m);
+void launch_inner_update(cudaStream_t st, int m, const double* u2, const double* s0u, const int* kptr,
+                         const int* kidx, const double* kval, const double* g, const double* pw, const double* v,
+                         const int* cptr, const int* csrc, double* f_tilde2, double* u2acc, double* x,
+                         const int* x2_ids, double* rpartial);
+void launch_scatter_add(cudaStream_t st, int cnt, const int* node, const double* X, double* x);
+void launch_gather3(cudaStream_t st, int cnt, const int* idx, const double* src, double* out);
+int attachment_blocks(int na);
+void launch_attachment_energy(cudaStream_t st, int na, const int* nodes, const double* k, const double* tgt,
+                              const double* x, double* partial);
+void launch_finish_metrics(cudaStream_t st, const double* e_part, int ne_b, const double* a_part, int na_b,
+                           const double* p_part, int np_b, const double* r_part, int nr_b, const uint8_t* active,
+                           int P, int have_residual, double* out);
+
+}  // namespace spb
