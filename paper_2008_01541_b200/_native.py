@@ -26,7 +26,7 @@ from .errors import (
 )
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libschurpd_b200.so"
+LIB_PATH = PKG / "lib" / os.environ.get("SPB_LIB_NAME", "libschurpd_b200.so")
 CSRC = PKG / "csrc"
 
 SPB_OK, SPB_ERR_ARG, SPB_ERR_INDEFINITE, SPB_ERR_PARTITION, SPB_ERR_SETUP, SPB_ERR_CUDA, SPB_ERR_ALLOC = range(7)

@@ -200,12 +200,12 @@ __global__ void __launch_bounds__(256) k_build_g(int m, const double* __restrict
   g[3 * k + 1] = g1;
   g[3 * k + 2] = g2;
   if (ytile) {
-    // tile j = k/64 of the RHS row holds g^T: element (r, c) at r*64 + c
+    // tile j = k/64 of the RHS row holds g^T (rows 0..2, swizzled layout)
     int tj = k >> 6, c = k & 63;
     double* t = ytile + (int64_t)tj * 4096;
-    t[0 * 64 + c] = g0;
-    t[1 * 64 + c] = g1;
-    t[2 * 64 + c] = g2;
+    t[swz(0, c)] = g0;
+    t[swz(1, c)] = g1;
+    t[swz(2, c)] = g2;
   }
 }
 

@@ -74,4 +74,17 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
+// Dense 64x64 FP64 tiles are stored "swizzled row-major": element (r, c) at
+// r*64 + (c ^ ((r & 3) << 2)). The XOR moves 4-column groups so that DMMA
+// fragment loads (8 rows x 4 consecutive k) hit 16 distinct 8-byte bank slots
+// per half-warp, while whole tiles stay contiguous for 1D bulk (TMA) copies.
+__host__ __device__ __forceinline__ int swz(int r, int c) { return r * 64 + (c ^ ((r & 3) << 2)); }
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 }  // namespace spb

@@ -126,7 +126,7 @@ struct Ctx {
   DBuf<double> k_val;
   // dense
   int N = 0, ntasks = 0;
-  DBuf<double> sigma0_tiles, L, Linv, Y, gemv_partial, xrows;
+  DBuf<double> sigma0_tiles, L, LinvT, Y, gemv_partial, xrows;
   DBuf<int> flags, counter, info, xflags;
   DBuf<int2> tasks;
   DBuf<int> c22_tile_ptr, c22_ent_rc, c22_ent_ptr, c22_contrib;
@@ -302,12 +302,12 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
             double v = 0.0;
             if (gr < n2 && gcc < n2) v = f->sigma0[(size_t)gr * n2 + gcc];
             else if (gr == gcc) v = 1.0;
-            T[r * 64 + c] = v;
+            T[swz(r, c)] = v;
           }
       }
     TRY(sigma0_tiles.upload(tiles));
     TRY(L.zeros((size_t)nt * 4096));
-    TRY(Linv.zeros((size_t)N * 4096));
+    TRY(LinvT.zeros((size_t)N * 4096));
     TRY(Y.zeros((size_t)N * 4096));
     TRY(flags.zeros(nt + N));
     TRY(counter.zeros(1));
@@ -315,11 +315,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
     TRY(xflags.zeros(N));
     TRY(xrows.zeros((size_t)N * 3 * 64));
     TRY(gemv_partial.zeros((size_t)nt * 6 * 64));
-    std::vector<int2> tk;
-    for (int j = 0; j < N; ++j) {
-      for (int i = j; i < N; ++i) tk.push_back(make_int2(i, j));
-      tk.push_back(make_int2(N, j));
-    }
+    std::vector<int2> tk = cholesky_task_order(N, true, CHOL_LEAD);
     ntasks = (int)tk.size();
     TRY(tasks.upload(tk));
     // C22 entries: upper (c, r) COO contributions in (proxy, a, b) order, stored at
@@ -348,7 +344,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
     TRY(c22_ent_rc.upload(erc));
     TRY(c22_ent_ptr.upload(eptr));
     TRY(c22_contrib.upload(codes));
-    dd = DenseDev{n2, N, sigma0_tiles.p, L.p, Linv.p, Y.p, flags.p, counter.p, info.p,
+    dd = DenseDev{n2, N, sigma0_tiles.p, L.p, LinvT.p, Y.p, flags.p, counter.p, info.p,
                   c22_tile_ptr.p, c22_ent_rc.p, c22_ent_ptr.p, c22_contrib.p, prox_w.p, prox_c.p, active.p};
   }
   // colliders + metrics
@@ -418,7 +414,7 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
       SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
       SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
       SPB_CUDA(cudaMemsetAsync(xflags.p, 0, sizeof(int) * N, st));
-      launch_cholesky_tiles(st, dd, tasks.p, ntasks, NUM_SMS_B200);
+      launch_cholesky_tiles(st, dd, tasks.p, ntasks, std::min(NUM_SMS_B200, ntasks));
       launch_dense_backward(st, dd, xflags.p, xrows.p, u2.p);
       // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual
       launch_sym_tile_gemv(st, dd, u2.p, gemv_partial.p);
@@ -699,11 +695,15 @@ int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
   SPB_CUDA(cudaEventCreate(&e0));
   SPB_CUDA(cudaEventCreate(&e1));
   float tot = 0;
+  // SPB_CHOL_NODEPS=1 (diagnostics only): every readiness flag preset, so the
+  // launch measures raw task throughput without dependency waits (result invalid).
+  const char* nd = getenv("SPB_CHOL_NODEPS");
+  const int preset = (nd && nd[0] == '1') ? 1 : 0;
   for (int r = 0; r < reps; ++r) {
-    SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
+    SPB_CUDA(cudaMemsetAsync(c->flags.p, preset, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
     SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
     SPB_CUDA(cudaEventRecord(e0, c->st));
-    spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, spb::NUM_SMS_B200);
+    spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
     SPB_CUDA(cudaEventRecord(e1, c->st));
     SPB_CUDA(cudaEventSynchronize(e1));
     float ms1;

@@ -2,66 +2,105 @@
 // PAPER.md:402-441; reference linalg.py:432-461 + solver.py:430-440).
 //
 //   k_cholesky_tiles   H = sigma0 + C22 assembled on the fly and factored
-//                      LL^T in ONE persistent launch: left-looking 64x64 tile
-//                      tasks claimed in dependency order, per-tile readiness
-//                      flags (acquire/release), trailing products on the FP64
-//                      tensor pipe (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4;
-//                      tcgen05 has no f64 kind). The RHS g rides along as an
-//                      extra tile ROW of the matrix, so the forward
-//                      substitution y = L^-1 g is produced by the same tasks.
+//                      LL^T in ONE persistent launch over 64x64 tiles:
+//                      left-looking tile tasks claimed from a global counter
+//                      in dependency order (diagonal tasks claimed LEAD columns
+//                      ahead), per-tile readiness flags (release / relaxed poll
+//                      + acquire fence). Per CTA a producer warp streams the
+//                      (L_ik, L_jk) tile pairs with 1D bulk async copies (TMA)
+//                      into a 3-stage mbarrier ring while 8 consumer warps run
+//                      the trailing products on the FP64 tensor pipe
+//                      (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4; tcgen05 has no
+//                      f64 kind). The RHS g rides along as an extra tile ROW,
+//                      so y = L^-1 g comes out of the same tasks. Diagonal
+//                      tiles are factored register-resident as the augmented
+//                      panel [A; I], giving L_jj and L_jj^-T in one sweep.
 //   k_dense_backward   u = L^-T y, one CTA per tile column, flag chained.
-//   k_sym_gemv_*       sigma0 u (symmetric, lower tiles read once) for the
-//                      f~2 maintenance and the residual (solver.py:436-440).
+//   k_sym_gemv_*       sigma0 u (lower tiles read once) for the f~2 upkeep
+//                      and the residual (solver.py:436-440).
 //
-// Layout: tile (i,j), i >= j, at index i(i+1)/2 + j, 64x64 row-major. The
-// order m is padded to 64 N with an identity tail.
+// Layout: tile (i,j), i >= j, at index i(i+1)/2 + j; 64x64 swizzled row-major
+// (common.cuh swz). The order m is padded to 64 N with an identity tail.
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace spb {
 
-constexpr int TS = 64;     // tile size
-constexpr int LDS = 68;    // padded smem row (8-byte bank slots (4g+t) mod 16 distinct)
-constexpr int TILE_SMEM = TS * LDS;
+constexpr int TS = 64;
+constexpr int TILE = TS * TS;            // doubles per tile
+constexpr int TILE_BYTES = TILE * 8;     // 32 KB
+constexpr int NSTAGE = 3;
+constexpr int NCONS = 256;               // consumer threads (8 warps)
+constexpr int NTHREADS = NCONS + 32;     // + 1 producer warp
+constexpr int LDP = 66;                  // plain row stride of the potrf scratch
+#ifndef SPB_CHOL_CPASYNC
+#define SPB_CHOL_CPASYNC 0               // 1: generic-proxy cp.async producer instead of bulk TMA
+#endif
 
 __host__ __device__ __forceinline__ int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
 int dense_tile_count(int N) { return N * (N + 1) / 2; }
-size_t cholesky_smem_bytes() { return sizeof(double) * (4 * TILE_SMEM + 2 * TS) + 16; }
 
+struct CholSmem {
+  double stage[NSTAGE][2][TILE];
+  double col[2][128];
+  double ipiv[2];
+  unsigned long long full[NSTAGE];
+  unsigned long long empty[NSTAGE];
+  int task;
+};
+size_t cholesky_smem_bytes() { return sizeof(CholSmem) + 128; }
+
+// ------------------------------------------------------------- primitives
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
-
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, int bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, int parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n }\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, int bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCONS) : "memory"); }
 
-// global tile (row-major 64x64) -> smem tile (row stride LDS), 256 threads
-__device__ __forceinline__ void load_tile_async(double* s, const double* g) {
-  for (int q = threadIdx.x; q < TS * TS / 2; q += blockDim.x) {
-    int r = q >> 5, c2 = (q & 31) * 2;
-    cp_async16(s + r * LDS + c2, g + r * TS + c2);
+// Spin (one thread) until a readiness flag is set, then order later reads
+// (generic and async proxy) after the producer's release.
+__device__ __forceinline__ void poll_flag(const int* f) {
+  if (ld_relaxed(f) == 0) {
+    while (ld_relaxed(f) == 0) __nanosleep(32);
   }
+  fence_acq_rel_gpu();
+  fence_proxy_async_global();
 }
 
-__device__ __forceinline__ void wait_flag(const int* f) {
-  if (threadIdx.x == 0) {
-    while (ld_acquire(f) == 0) __nanosleep(64);
-  }
-  __syncthreads();
-}
-
-// Warp tile: 32 rows x 16 cols; 8 warps cover 64x64 as 2 (rows) x 4 (cols).
+// Warp tile 32 rows x 16 cols; 8 warps cover 64x64 as 2 x 4.
 struct Acc {
   double c[4][2][2];
 };
-
 __device__ __forceinline__ void acc_zero(Acc& a) {
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb)
@@ -69,20 +108,20 @@ __device__ __forceinline__ void acc_zero(Acc& a) {
     for (int nb = 0; nb < 2; ++nb) a.c[mb][nb][0] = a.c[mb][nb][1] = 0.0;
 }
 
-// acc += sign * A * B^T over K = 64, A and B row-major 64x64 smem tiles.
+// acc (+/-)= A * B^T, A and B swizzled 64x64 (rows of B are the n index).
 template <bool NEG>
-__device__ __forceinline__ void tile_gemm_abt(Acc& acc, const double* sA, const double* sB, int wr, int wc,
-                                              int lane) {
+__device__ __forceinline__ void mma_abt(Acc& acc, const double* sA, const double* sB, int wr, int wc, int lane) {
   const int g = lane >> 2, t = lane & 3;
-  const double* pa = sA + (wr * 32 + g) * LDS + t;
-  const double* pb = sB + (wc * 16 + g) * LDS + t;
 #pragma unroll 4
   for (int kk = 0; kk < TS; kk += 4) {
     double a[4], b[2];
 #pragma unroll
-    for (int mb = 0; mb < 4; ++mb) a[mb] = NEG ? -pa[mb * 8 * LDS + kk] : pa[mb * 8 * LDS + kk];
+    for (int mb = 0; mb < 4; ++mb) {
+      double v = sA[swz(wr * 32 + mb * 8 + g, kk + t)];
+      a[mb] = NEG ? -v : v;
+    }
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) b[nb] = pb[nb * 8 * LDS + kk];
+    for (int nb = 0; nb < 2; ++nb) b[nb] = sB[swz(wc * 16 + nb * 8 + g, kk + t)];
 #pragma unroll
     for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
@@ -90,99 +129,56 @@ __device__ __forceinline__ void tile_gemm_abt(Acc& acc, const double* sA, const 
   }
 }
 
-// fragment <-> smem tile (row stride LDS)
-__device__ __forceinline__ void acc_to_smem(const Acc& acc, double* s, int wr, int wc, int lane) {
+// acc += A * B, A swizzled 64x64 (M x K), B swizzled 64x64 row-major (K x N).
+__device__ __forceinline__ void mma_ab(Acc& acc, const double* sA, const double* sB, int wr, int wc, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll 4
+  for (int kk = 0; kk < TS; kk += 4) {
+    double a[4], b[2];
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb) a[mb] = sA[swz(wr * 32 + mb * 8 + g, kk + t)];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) b[nb] = sB[swz(kk + t, wc * 16 + nb * 8 + g)];
+#pragma unroll
+    for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], a[mb], b[nb]);
+  }
+}
+
+// fragment (row r0+g, cols c0+2t, c0+2t+1) <-> swizzled tile
+template <typename F>
+__device__ __forceinline__ void acc_foreach(int wr, int wc, int lane, F f) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      int r = wr * 32 + mb * 8 + g, c = wc * 16 + nb * 8 + 2 * t;
-      s[r * LDS + c] = acc.c[mb][nb][0];
-      s[r * LDS + c + 1] = acc.c[mb][nb][1];
-    }
+    for (int nb = 0; nb < 2; ++nb) f(mb, nb, wr * 32 + mb * 8 + g, wc * 16 + nb * 8 + 2 * t);
 }
 __device__ __forceinline__ void smem_to_acc(Acc& acc, const double* s, int wr, int wc, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int mb = 0; mb < 4; ++mb)
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      int r = wr * 32 + mb * 8 + g, c = wc * 16 + nb * 8 + 2 * t;
-      acc.c[mb][nb][0] = s[r * LDS + c];
-      acc.c[mb][nb][1] = s[r * LDS + c + 1];
-    }
+  acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
+    double2 v = *reinterpret_cast<const double2*>(s + swz(r, c));
+    acc.c[mb][nb][0] = v.x;
+    acc.c[mb][nb][1] = v.y;
+  });
 }
-__device__ __forceinline__ void acc_to_global(const Acc& acc, double* gt, int wr, int wc, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int mb = 0; mb < 4; ++mb)
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
-      int r = wr * 32 + mb * 8 + g, c = wc * 16 + nb * 8 + 2 * t;
-      *reinterpret_cast<double2*>(gt + r * TS + c) = make_double2(acc.c[mb][nb][0], acc.c[mb][nb][1]);
-    }
+__device__ __forceinline__ void acc_to_swz(const Acc& acc, double* s, int wr, int wc, int lane) {
+  acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
+    *reinterpret_cast<double2*>(s + swz(r, c)) = make_double2(acc.c[mb][nb][0], acc.c[mb][nb][1]);
+  });
+}
+__device__ __forceinline__ void acc_to_plain(const Acc& acc, double* s, int wr, int wc, int lane) {
+  acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
+    s[r * LDP + c] = acc.c[mb][nb][0];
+    s[r * LDP + c + 1] = acc.c[mb][nb][1];
+  });
 }
 
-// In-smem Cholesky of a 64x64 SPD tile (lower), then its triangular inverse.
-// Writes L (strict upper zeroed) and inv(L) to global. Returns via *info the
-// 1-based global column of the first non-positive pivot (dpotrf semantics).
-__device__ void potrf_inv_tile(double* S, double* col, double* gL, double* gLinv, int j, int* info) {
-  const int tid = threadIdx.x;
-  for (int k = 0; k < TS; ++k) {
-    double d = S[k * LDS + k];
-    if (!(d > 0.0)) {
-      if (tid == 0) atomicCAS(info, 0, j * TS + k + 1);
-    }
-    double dk = sqrt(d);
-    if (tid > k && tid < TS) {
-      double l = S[tid * LDS + k] / dk;
-      col[tid] = l;
-      S[tid * LDS + k] = l;
-    }
-    __syncthreads();
-    if (tid == 0) S[k * LDS + k] = dk;
-    // trailing update of rows/cols > k (lower part)
-    const int rem = TS - 1 - k;
-    for (int q = tid; q < rem * rem; q += blockDim.x) {
-      int r = k + 1 + q / rem, c = k + 1 + q % rem;
-      if (c <= r) S[r * LDS + c] -= col[r] * col[c];
-    }
-    __syncthreads();
-  }
-  // write L (zero strict upper)
-  for (int q = tid; q < TS * TS; q += blockDim.x) {
-    int r = q >> 6, c = q & 63;
-    gL[q] = (c <= r) ? S[r * LDS + c] : 0.0;
-  }
-  // inverse: column c of X = L^-1 by forward substitution (one thread per column)
-  double* X = S + TS * LDS;  // second tile buffer (caller guarantees space)
-  if (tid < TS) {
-    const int c = tid;
-    for (int r = 0; r < TS; ++r) {
-      double v;
-      if (r < c) {
-        v = 0.0;
-      } else {
-        double s = (r == c) ? 1.0 : 0.0;
-        for (int k = c; k < r; ++k) s -= S[r * LDS + k] * X[k * LDS + c];
-        v = s / S[r * LDS + r];
-      }
-      X[r * LDS + c] = v;
-    }
-  }
-  __syncthreads();
-  for (int q = tid; q < TS * TS; q += blockDim.x) {
-    int r = q >> 6, c = q & 63;
-    gLinv[q] = X[r * LDS + c];
-  }
-}
-
-// Add C22 contributions of the active proxies to one tile held in smem
-// (contributions summed in the reference's COO order, then added: h = sigma0 + c22).
+// Add the active proxies' C22 entries of one tile (swizzled smem). Each entry
+// sums its contributions in the reference's COO order, then h = sigma0 + c22.
 __device__ __forceinline__ void add_c22(const DenseDev& d, int tile, double* S) {
   int e0 = d.c22_tile_ptr[tile], e1 = d.c22_tile_ptr[tile + 1];
-  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+  for (int e = e0 + (int)threadIdx.x; e < e1; e += NCONS) {
     double s = 0.0;
     bool any = false;
     for (int q = d.c22_ent_ptr[e]; q < d.c22_ent_ptr[e + 1]; ++q) {
@@ -195,103 +191,257 @@ __device__ __forceinline__ void add_c22(const DenseDev& d, int tile, double* S) 
     }
     if (any) {
       int rc = d.c22_ent_rc[e];
-      S[(rc >> 6) * LDS + (rc & 63)] += s;
+      S[swz(rc >> 6, rc & 63)] += s;
     }
   }
 }
 
-__global__ void __launch_bounds__(256, 1) k_cholesky_tiles(DenseDev d, const int2* __restrict__ tasks, int ntasks) {
-  extern __shared__ __align__(16) double smem[];
-  double* sA[2] = {smem, smem + TILE_SMEM};
-  double* sB[2] = {smem + 2 * TILE_SMEM, smem + 3 * TILE_SMEM};
-  double* col = smem + 4 * TILE_SMEM;
-  __shared__ int s_task;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// ------------------------------------------------ diagonal tile factorization
+// Register-resident right-looking Cholesky of the augmented 128 x 64 panel
+// [A; I]: thread (row r in [0,128), half h) holds columns 32h..32h+31 of row r.
+// One consumer barrier per column; column k+1 is computed one step ahead and
+// the pivot of column k+2 is published early (look-ahead), so the rsqrt latency
+// overlaps the trailing update. Rows 0..63 end as L_jj (lower), rows 64..127
+// as L_jj^-T (upper).
+template <int H>
+__device__ __forceinline__ void potrf_steps(double (&a)[32], int r, CholSmem& sm, int j, int* info) {
+  constexpr int C0 = 32 * H;
+#pragma unroll
+  for (int k = 0; k < 63; ++k) {
+    const int k1 = k + 1, k2 = k + 2;
+    if (k == 31) {
+      // cross-half pivot of column 32: its row-32 owner (half 1) needs L[32][31]
+      if (H == 1 && r == 32) {
+        double l = sm.col[1][32];
+        double d = a[0] - l * l;
+        if (!(d > 0.0)) atomicCAS(info, 0, j * TS + 32 + 1);
+        a[0] = d;
+        sm.ipiv[0] = rsqrt(d);
+      }
+      cons_sync();
+    }
+    if (r > k) {
+      const double* colk = sm.col[k & 1];
+      const double lr = colk[r];
+      // 1) column k+1 first (look-ahead), then L[:, k+1] in its owner half
+      if (k1 >= C0 && k1 < C0 + 32) {
+        const int q1 = (k + 1) & 31;
+        const bool pub_done = (r == k1);  // its pivot publish already applied columns k-1, k (or k at 31)
+        if (!pub_done) a[q1] -= lr * colk[k1];
+        const double ip = sm.ipiv[k1 & 1];
+        if (r == k1) {
+          a[q1] = a[q1] * ip;  // L_kk = d * rsqrt(d)
+        } else {
+          const double l1 = a[q1] * ip;
+          a[q1] = l1;
+          sm.col[k1 & 1][r] = l1;
+          // 2) publish the pivot of column k+2 (same half as column k+1)
+          if (r == k2 && k2 < 64 && (k2 >> 5) == H && (k1 >> 5) == H) {
+            const int q2 = (k + 2) & 31;
+            double d = a[q2] - lr * colk[k2];
+            d = d - l1 * l1;
+            if (!(d > 0.0)) atomicCAS(info, 0, j * TS + k2 + 1);
+            a[q2] = d;
+            sm.ipiv[k2 & 1] = rsqrt(d);
+          }
+        }
+      }
+      // 3) the rest of column k's update
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const int c = C0 + q;
+        if (c <= k1) continue;
+        const bool published = (c == k2) && (r == k2) && ((k2 >> 5) == H) && ((k1 >> 5) == H);
+        if (!published) a[q] -= lr * colk[c];
+      }
+    }
+    cons_sync();
+  }
+}
+
+__device__ void potrf_aug_tile(const Acc& acc, CholSmem& sm, double* scratch, double* gL, double* gLinvT, int j,
+                               int* info, int wr, int wc, int lane) {
+  const int tid = threadIdx.x;
+  cons_sync();  // every warp has finished reading the scratch stage
+  acc_to_plain(acc, scratch, wr, wc, lane);
+  cons_sync();
+  const int h = tid >> 7, r = tid & 127;
+  double a[32];
+  if (r < 64) {
+#pragma unroll
+    for (int q = 0; q < 32; q += 2) {
+      double2 v = *reinterpret_cast<const double2*>(scratch + r * LDP + 32 * h + q);
+      a[q] = v.x;
+      a[q + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) a[q] = (32 * h + q == r - 64) ? 1.0 : 0.0;
+  }
+  cons_sync();  // scratch reads done before the prologue writes col[]
+  // prologue: pivot 0, column 0, pivot 1
+  if (h == 0 && r == 0) {
+    double d = a[0];
+    if (!(d > 0.0)) atomicCAS(info, 0, j * TS + 1);
+    sm.ipiv[0] = rsqrt(d);
+  }
+  cons_sync();
+  if (h == 0) {
+    const double ip = sm.ipiv[0];
+    if (r == 0) {
+      a[0] = a[0] * ip;
+    } else {
+      const double l = a[0] * ip;
+      a[0] = l;
+      sm.col[0][r] = l;
+      if (r == 1) {
+        double d = a[1] - l * l;
+        if (!(d > 0.0)) atomicCAS(info, 0, j * TS + 2);
+        a[1] = d;
+        sm.ipiv[1] = rsqrt(d);
+      }
+    }
+  }
+  cons_sync();
+  if (h == 0) potrf_steps<0>(a, r, sm, j, info);
+  else potrf_steps<1>(a, r, sm, j, info);
+  // write L_jj (zero strict upper) and L_jj^-T
+  if (r < 64) {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int c = 32 * h + q;
+      gL[swz(r, c)] = (c <= r) ? a[q] : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 32; ++q) gLinvT[swz(r - 64, 32 * h + q)] = a[q];
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, const int2* __restrict__ tasks,
+                                                                int ntasks) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  CholSmem& sm = *reinterpret_cast<CholSmem*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp == 8;
   const int wr = warp >> 2, wc = warp & 3;
   const int N = d.N;
   const int ntiles = N * (N + 1) / 2;
-
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm.full[s], SPB_CHOL_CPASYNC ? 32 : 1);
+      mbar_init(&sm.empty[s], NCONS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int it = 0;  // stage-use counter, advanced identically by producer and consumers
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(d.counter, 1);
+    if (tid == 0) sm.task = atomicAdd(d.counter, 1);
     __syncthreads();
-    const int task = s_task;
-    __syncthreads();
+    const int task = sm.task;
     if (task >= ntasks) break;
     const int2 ij = tasks[task];
     const int i = ij.x, j = ij.y;
     const bool rhs = (i == N);
-    const double* src = rhs ? d.Y + (int64_t)j * TS * TS : d.sigma0 + (int64_t)tidx(i, j) * TS * TS;
-
-    // ---- acc <- H tile (sigma0 + C22) or g^T tile
-    Acc acc;
-    load_tile_async(sA[0], src);
-    cp_async_commit();
-    cp_async_wait_all();
-    __syncthreads();
-    if (!rhs && d.c22_tile_ptr) {
-      add_c22(d, tidx(i, j), sA[0]);
-      __syncthreads();
-    }
-    smem_to_acc(acc, sA[0], wr, wc, lane);
-    __syncthreads();
-
-    // ---- left-looking accumulation over k < j, double-buffered
-    if (j > 0) {
-      auto fa = [&](int k) -> const int* { return d.flags + (rhs ? ntiles + k : tidx(i, k)); };
-      auto ta = [&](int k) -> const double* {
-        return rhs ? d.Y + (int64_t)k * TS * TS : d.L + (int64_t)tidx(i, k) * TS * TS;
-      };
-      wait_flag(fa(0));
-      wait_flag(d.flags + tidx(j, 0));
-      load_tile_async(sA[0], ta(0));
-      load_tile_async(sB[0], d.L + (int64_t)tidx(j, 0) * TS * TS);
-      cp_async_commit();
-      for (int k = 0; k < j; ++k) {
-        const int cur = k & 1;
-        if (k + 1 < j) {
-          wait_flag(fa(k + 1));
-          wait_flag(d.flags + tidx(j, k + 1));
-          load_tile_async(sA[cur ^ 1], ta(k + 1));
-          load_tile_async(sB[cur ^ 1], d.L + (int64_t)tidx(j, k + 1) * TS * TS);
-          cp_async_commit();
-          cp_async_wait_1();
-        } else {
-          cp_async_wait_all();
-        }
-        __syncthreads();
-        tile_gemm_abt<true>(acc, sA[cur], sB[cur], wr, wc, lane);
-        __syncthreads();
-      }
-    }
-
-    // ---- finalize
     int* myflag = d.flags + (rhs ? ntiles + j : tidx(i, j));
-    if (i == j) {
-      acc_to_smem(acc, sA[0], wr, wc, lane);
-      __syncthreads();
-      // sA[0] holds S, sA[1] is scratch for the inverse
-      potrf_inv_tile(sA[0], col, d.L + (int64_t)tidx(j, j) * TS * TS, d.Linv + (int64_t)j * TS * TS, j, d.info);
+
+    if (producer) {
+      // the whole producer warp walks the task; lane 0 polls flags / waits for
+      // free stages, then the tiles are streamed into the stage ring
+      auto fill = [&](const double* a, const double* b, int slot_a) {
+        const int s = it % NSTAGE;
+        if (lane == 0) mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
+        __syncwarp();
+#if SPB_CHOL_CPASYNC
+        // generic-proxy path: 16-byte cp.async per lane, completion tracked on
+        // full[s] by one noinc arrive per lane (count 32)
+        for (int q = lane; q < TILE / 2; q += 32) cp_async16(sm.stage[s][slot_a] + 2 * q, a + 2 * q);
+        if (b)
+          for (int q = lane; q < TILE / 2; q += 32) cp_async16(sm.stage[s][1] + 2 * q, b + 2 * q);
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
+#else
+        if (lane == 0) {
+          mbar_expect_tx(&sm.full[s], (b ? 2 : 1) * TILE_BYTES);
+          bulk_g2s(sm.stage[s][slot_a], a, TILE_BYTES, &sm.full[s]);
+          if (b) bulk_g2s(sm.stage[s][1], b, TILE_BYTES, &sm.full[s]);
+        }
+#endif
+        ++it;
+      };
+      auto wait_ready = [&](const int* f) {
+        if (lane == 0) poll_flag(f);
+        __syncwarp();
+      };
+      const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
+      fill(src, nullptr, 0);
+      for (int k = 0; k < j; ++k) {
+        wait_ready(d.flags + (rhs ? ntiles + k : tidx(i, k)));
+        wait_ready(d.flags + tidx(j, k));
+        fill(rhs ? d.Y + (size_t)k * TILE : d.L + (size_t)tidx(i, k) * TILE, d.L + (size_t)tidx(j, k) * TILE, 0);
+      }
+      if (i != j) {
+        wait_ready(d.flags + tidx(j, j));
+        fill(d.LinvT + (size_t)j * TILE, nullptr, 1);
+      }
     } else {
-      wait_flag(d.flags + tidx(j, j));
-      load_tile_async(sB[0], d.Linv + (int64_t)j * TS * TS);
-      cp_async_commit();
-      acc_to_smem(acc, sA[0], wr, wc, lane);
-      cp_async_wait_all();
-      __syncthreads();
-      Acc out;
-      acc_zero(out);
-      tile_gemm_abt<false>(out, sA[0], sB[0], wr, wc, lane);  // acc * inv(Ljj)^T
-      double* dst = rhs ? d.Y + (int64_t)j * TS * TS : d.L + (int64_t)tidx(i, j) * TS * TS;
-      acc_to_global(out, dst, wr, wc, lane);
+      // ---- consumers: acc <- H tile (sigma0 + C22) or the g^T tile
+      Acc acc;
+      int s = it % NSTAGE;
+      mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+      if (!rhs && d.c22_tile_ptr) {
+        add_c22(d, tidx(i, j), sm.stage[s][0]);
+        cons_sync();
+      }
+      smem_to_acc(acc, sm.stage[s][0], wr, wc, lane);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      int last = s;
+      ++it;
+      // ---- left-looking accumulation over k < j
+      for (int k = 0; k < j; ++k) {
+        s = it % NSTAGE;
+        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+        mma_abt<true>(acc, sm.stage[s][0], sm.stage[s][1], wr, wc, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        last = s;
+        ++it;
+      }
+      // ---- finalize
+      if (i == j) {
+        // stages are idle until the next task: use the last one as scratch
+        potrf_aug_tile(acc, sm, sm.stage[last][0], d.L + (size_t)tidx(j, j) * TILE, d.LinvT + (size_t)j * TILE, j,
+                       d.info, wr, wc, lane);
+      } else {
+        double* scratch = sm.stage[last][0];
+        cons_sync();  // every warp has finished reading stage `last`
+        acc_to_swz(acc, scratch, wr, wc, lane);
+        cons_sync();
+        s = it % NSTAGE;
+        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+        Acc out;
+        acc_zero(out);
+        mma_ab(out, scratch, sm.stage[s][1], wr, wc, lane);  // acc * inv(L_jj)^T = acc * LinvT
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        ++it;
+        double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
+        acc_to_swz(out, dst, wr, wc, lane);
+      }
+      fence_proxy_async_smem();    // generic smem writes before later bulk copies into the stages
+      fence_proxy_async_global();  // generic global tile stores before other CTAs' bulk reads
+      __threadfence();
     }
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) st_release(myflag, 1);
+    if (tid == 0) st_release(myflag, 1);
   }
 }
 
 // u = L^-T y: x_j^T = (y_j^T - sum_{i>j} x_i^T L_ij) inv(L_jj). CTA b handles
-// block j = N-1-b; blocks only wait on lower CTA indices.
+// block j = N-1-b and only waits on lower CTA indices.
 __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, int* __restrict__ xflags,
                                                         double* __restrict__ xrows /* N*3*64 */,
                                                         double* __restrict__ u, int m) {
@@ -300,29 +450,33 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, int* __restr
   const int N = d.N;
   const int j = N - 1 - blockIdx.x;
   const int tid = threadIdx.x;
-  const int r = tid >> 6, c = tid & 63;  // r < 3 valid (192 threads)
+  const int r = tid >> 6, c = tid & 63;  // r < 3 active (192 threads)
   double acc = 0.0;
   for (int i = N - 1; i > j; --i) {
-    wait_flag(xflags + i);
-    if (tid < 3 * TS) xi[tid] = xrows[(int64_t)i * 3 * TS + tid];
+    if (tid == 0) {
+      while (ld_relaxed(xflags + i) == 0) __nanosleep(32);
+      fence_acq_rel_gpu();
+    }
+    __syncthreads();
+    if (tid < 3 * TS) xi[tid] = __ldcg(xrows + (size_t)i * 3 * TS + tid);
     __syncthreads();
     if (r < 3) {
-      const double* L = d.L + (int64_t)tidx(i, j) * TS * TS;
+      const double* L = d.L + (size_t)tidx(i, j) * TILE;
       double s = 0.0;
 #pragma unroll 8
-      for (int k = 0; k < TS; ++k) s += xi[r * TS + k] * L[k * TS + c];
+      for (int k = 0; k < TS; ++k) s += xi[r * TS + k] * L[swz(k, c)];
       acc += s;
     }
     __syncthreads();
   }
-  if (r < 3) acc_s[r * TS + c] = d.Y[(int64_t)j * TS * TS + r * TS + c] - acc;
+  if (r < 3) acc_s[r * TS + c] = d.Y[(size_t)j * TILE + swz(r, c)] - acc;
   __syncthreads();
   if (r < 3) {
-    const double* Li = d.Linv + (int64_t)j * TS * TS;
+    const double* LiT = d.LinvT + (size_t)j * TILE;  // x = tmp * inv(L_jj) = tmp * LinvT^T
     double s = 0.0;
 #pragma unroll 8
-    for (int k = 0; k < TS; ++k) s += acc_s[r * TS + k] * Li[k * TS + c];
-    xrows[(int64_t)j * 3 * TS + r * TS + c] = s;
+    for (int k = 0; k < TS; ++k) s += acc_s[r * TS + k] * LiT[swz(c, k)];
+    xrows[(size_t)j * 3 * TS + r * TS + c] = s;
     int row = j * TS + c;
     if (row < m) u[3 * row + r] = s;
   }
@@ -335,7 +489,6 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, int* __restr
 __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double* __restrict__ u,
                                                         double* __restrict__ partial) {
   const int t = blockIdx.x;
-  // decode tile (i, j)
   int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
   while (tidx(i + 1, 0) <= t) ++i;
   while (tidx(i, 0) > t) --i;
@@ -353,14 +506,13 @@ __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double
     }
   }
   __syncthreads();
-  const double* T = d.sigma0 + (int64_t)t * TS * TS;
-  // row contribution: warp w handles rows w*8..w*8+7, lanes over columns
+  const double* T = d.sigma0 + (size_t)t * TILE;
   const int lane = tid & 31, w = tid >> 5;
-  double* out_row = partial + (int64_t)t * 2 * 3 * TS;
+  double* out_row = partial + (size_t)t * 6 * TS;
   double* out_col = out_row + 3 * TS;
   for (int rr = 0; rr < 8; ++rr) {
     int row = w * 8 + rr;
-    double a0 = T[row * TS + lane], a1 = T[row * TS + lane + 32];
+    double a0 = T[swz(row, lane)], a1 = T[swz(row, lane + 32)];
     double s0 = a0 * uj[lane] + a1 * uj[lane + 32];
     double s1 = a0 * uj[TS + lane] + a1 * uj[TS + lane + 32];
     double s2 = a0 * uj[2 * TS + lane] + a1 * uj[2 * TS + lane + 32];
@@ -374,11 +526,10 @@ __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double
     }
   }
   if (i != j) {
-    // column contribution: T^T ui -> thread (cgrp, col): partial over 16 rows
     const int cc = tid & 63, grp = tid >> 6;
     double s0 = 0, s1 = 0, s2 = 0;
     for (int rr = grp * 16; rr < grp * 16 + 16; ++rr) {
-      double a = T[rr * TS + cc];
+      double a = T[swz(rr, cc)];
       s0 += a * ui[rr];
       s1 += a * ui[TS + rr];
       s2 += a * ui[2 * TS + rr];
@@ -392,13 +543,12 @@ __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double
 }
 
 __global__ void k_sym_gemv_reduce(DenseDev d, const double* __restrict__ partial, double* __restrict__ out) {
-  // block b: out rows b*64..; sum row parts (b, j<=b) then column parts (i>b, b)
   const int b = blockIdx.x, tid = threadIdx.x;
   if (tid >= 3 * TS) return;
   const int q = tid / TS, r = tid % TS;
   double s = 0.0;
-  for (int j = 0; j <= b; ++j) s += partial[(int64_t)tidx(b, j) * 6 * TS + q * TS + r];
-  for (int i = b + 1; i < d.N; ++i) s += partial[(int64_t)tidx(i, b) * 6 * TS + 3 * TS + q * TS + r];
+  for (int j = 0; j <= b; ++j) s += partial[(size_t)tidx(b, j) * 6 * TS + q * TS + r];
+  for (int i = b + 1; i < d.N; ++i) s += partial[(size_t)tidx(i, b) * 6 * TS + 3 * TS + q * TS + r];
   int row = b * TS + r;
   if (row < d.m) out[3 * row + q] = s;
 }
@@ -411,7 +561,7 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
     cudaFuncSetAttribute(k_cholesky_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_cholesky_tiles<<<grid, 256, smem, st>>>(d, tasks, ntasks);
+  k_cholesky_tiles<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
 }
 
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, int* xflags, double* xrows, double* u) {
@@ -424,6 +574,26 @@ void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, d
 
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out) {
   k_sym_gemv_reduce<<<d.N, 192, 0, st>>>(d, partial, out);
+}
+
+// Task order: column-major (diag, below-diagonal tiles, RHS row), with each
+// diagonal task claimed `lead` columns ahead of its column so its long serial
+// accumulation overlaps the preceding columns. At most lead+1 claimed tasks
+// wait on unclaimed ones, so any grid larger than lead+1 CTAs (or holding all
+// tasks) cannot deadlock.
+std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead) {
+  if (const char* e = getenv("SPB_CHOL_LEAD")) lead = atoi(e);  // diagnostics override
+  std::vector<int2> tk;
+  int next_diag = 0;
+  for (int j = 0; j < N; ++j) {
+    while (next_diag < N && next_diag <= j + lead) {
+      tk.push_back(make_int2(next_diag, next_diag));
+      ++next_diag;
+    }
+    for (int i = j + 1; i < N; ++i) tk.push_back(make_int2(i, j));
+    if (with_rhs) tk.push_back(make_int2(N, j));
+  }
+  return tk;
 }
 
 }  // namespace spb

@@ -1,6 +1,8 @@
 // Host-side launchers of the device kernels (one translation unit per family).
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace spb {
@@ -45,7 +47,7 @@ struct DenseDev {
   int m, N;                  // order and tile count (T = 64)
   const double* sigma0;      // lower tiles, tile-major (diagonal tiles full)
   double* L;                 // factor tiles
-  double* Linv;              // inverse diagonal tiles (N)
+  double* LinvT;             // transposed inverse diagonal tiles (N)
   double* Y;                 // RHS tile row (N tiles): rows 0..2 = g^T, then y^T
   int* flags;                // N(N+1)/2 + N readiness flags
   int* counter;              // task counter
@@ -63,6 +65,8 @@ struct DenseDev {
 int dense_tile_count(int N);
 size_t cholesky_smem_bytes();
 void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid);
+std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead);
+constexpr int CHOL_LEAD = 4;
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, int* xflags, double* xrows, double* u);
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial);
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out);

@@ -57,7 +57,7 @@ int pack_tiles(int64_t m, int N, const double* h, std::vector<double>& tiles) {
       for (int r = 0; r < 64; ++r)
         for (int c = 0; c < 64; ++c) {
           int64_t gr = i * 64 + r, gc = j * 64 + c;
-          T[r * 64 + c] = (gr < m && gc < m) ? h[gr * m + gc] : (gr == gc ? 1.0 : 0.0);
+          T[swz(r, c)] = (gr < m && gc < m) ? h[gr * m + gc] : (gr == gc ? 1.0 : 0.0);
         }
     }
   return SPB_OK;
@@ -285,9 +285,7 @@ int32_t spb_op_dense_factor(int64_t m, const double* h, double* chol, int64_t* i
   SPB_CUDA(cudaMemset(dcnt.p, 0, sizeof(int)));
   SPB_CUDA(cudaMemset(dinfo.p, 0, sizeof(int)));
   SPB_CUDA(cudaMemset(dY.p, 0, sizeof(double) * N * 4096));
-  std::vector<int2> tk;
-  for (int j = 0; j < N; ++j)
-    for (int i = j; i < N; ++i) tk.push_back(make_int2(i, j));
+  std::vector<int2> tk = cholesky_task_order(N, false, CHOL_LEAD);
   TMP(int2, dtk, tk.size());
   H2D(dtk.p, tk.data(), sizeof(int2) * tk.size());
   DenseDev d{(int)m, N, dS.p, dL.p, dLi.p, dY.p, dflags.p, dcnt.p, dinfo.p, nullptr, nullptr, nullptr, nullptr,
@@ -301,7 +299,8 @@ int32_t spb_op_dense_factor(int64_t m, const double* h, double* chol, int64_t* i
   for (int64_t r = 0; r < m; ++r)
     for (int64_t c = 0; c < m; ++c) {
       int i = (int)(r / 64), j = (int)(c / 64);
-      chol[r * m + c] = (c <= r) ? tiles[(size_t)(i * (i + 1) / 2 + j) * 4096 + (r % 64) * 64 + (c % 64)] : 0.0;
+      chol[r * m + c] =
+          (c <= r) ? tiles[(size_t)(i * (i + 1) / 2 + j) * 4096 + swz((int)(r % 64), (int)(c % 64))] : 0.0;
     }
   if (hinfo > 0) {
     *info = hinfo;
@@ -312,41 +311,41 @@ int32_t spb_op_dense_factor(int64_t m, const double* h, double* chol, int64_t* i
   SPB_GUARD_END
 }
 
+// Solve with a given lower factor: its tiles and the transposed inverses of its
+// diagonal tiles (host, O(N 64^3)) feed the device sweeps: the forward sweep is
+// the tile kernel's RHS-row tasks with every L tile marked ready, the backward
+// sweep is k_dense_backward.
 int32_t spb_op_dense_solve(int64_t m, const double* chol, int64_t nrhs, const double* g, double* out) {
   SPB_GUARD_BEGIN
   if (m <= 0 || nrhs <= 0) return SPB_OK;
-  // Factor tiles of the given chol: run the tile kernel on H = chol chol^T?
-  // No: we pack chol directly and only need the two sweeps. The forward sweep
-  // reuses the Cholesky kernel's RHS-row tasks by factoring nothing: instead
-  // pack L, its diagonal inverses, and run forward + backward tile sweeps.
   const int N = (int)((m + 63) / 64);
   const int nt = dense_tile_count(N);
+  std::vector<double> lower((size_t)m * m);
+  for (int64_t r = 0; r < m; ++r)
+    for (int64_t c = 0; c < m; ++c) lower[r * m + c] = (c <= r) ? chol[r * m + c] : 0.0;
   std::vector<double> tiles;
-  pack_tiles(m, N, chol, tiles);
-  // zero strict upper of diagonal tiles (chol is lower)
+  pack_tiles(m, N, lower.data(), tiles);
+  std::vector<double> linvT((size_t)N * 4096, 0.0);
+  std::vector<double> T(4096), X(4096);
   for (int i = 0; i < N; ++i) {
-    double* T = tiles.data() + (size_t)(i * (i + 1) / 2 + i) * 4096;
+    const double* Ts = tiles.data() + (size_t)(i * (i + 1) / 2 + i) * 4096;
     for (int r = 0; r < 64; ++r)
-      for (int c = r + 1; c < 64; ++c) T[r * 64 + c] = 0.0;
-  }
-  // H = L L^T in tiles is not needed: we re-factor H = chol chol^T? That would
-  // change roundoff; instead build Linv tiles on the host (64x64 triangular
-  // inverses, O(N 64^3)) and run the device sweeps.
-  std::vector<double> linv((size_t)N * 4096, 0.0);
-  for (int i = 0; i < N; ++i) {
-    const double* T = tiles.data() + (size_t)(i * (i + 1) / 2 + i) * 4096;
-    double* X = linv.data() + (size_t)i * 4096;
+      for (int c = 0; c < 64; ++c) T[r * 64 + c] = Ts[swz(r, c)];
+    std::fill(X.begin(), X.end(), 0.0);
     for (int c = 0; c < 64; ++c)
       for (int r = c; r < 64; ++r) {
         double s = (r == c) ? 1.0 : 0.0;
         for (int k = c; k < r; ++k) s -= T[r * 64 + k] * X[k * 64 + c];
         X[r * 64 + c] = s / T[r * 64 + r];
       }
+    double* D = linvT.data() + (size_t)i * 4096;
+    for (int r = 0; r < 64; ++r)
+      for (int c = 0; c < 64; ++c) D[swz(c, r)] = X[r * 64 + c];  // transpose
   }
   TMP(double, dL, (size_t)nt * 4096);
   H2D(dL.p, tiles.data(), sizeof(double) * tiles.size());
   TMP(double, dLi, (size_t)N * 4096);
-  H2D(dLi.p, linv.data(), sizeof(double) * linv.size());
+  H2D(dLi.p, linvT.data(), sizeof(double) * linvT.size());
   TMP(double, dY, (size_t)N * 4096);
   TMP(int, dflags, nt + N);
   TMP(int, dcnt, 1);
@@ -354,7 +353,6 @@ int32_t spb_op_dense_solve(int64_t m, const double* chol, int64_t nrhs, const do
   TMP(int, xflags, N);
   TMP(double, xrows, (size_t)N * 3 * 64);
   TMP(double, du, 3 * m);
-  // forward via the RHS-row tasks of the tile kernel with all L tiles marked ready
   std::vector<int2> tk;
   for (int j = 0; j < N; ++j) tk.push_back(make_int2(N, j));
   TMP(int2, dtk, tk.size());
@@ -368,7 +366,8 @@ int32_t spb_op_dense_solve(int64_t m, const double* chol, int64_t nrhs, const do
   for (int64_t c0 = 0; c0 < nrhs; c0 += 3) {
     std::fill(ytile.begin(), ytile.end(), 0.0);
     for (int64_t r = 0; r < m; ++r)
-      for (int q = 0; q < 3 && c0 + q < nrhs; ++q) ytile[(size_t)(r / 64) * 4096 + q * 64 + r % 64] = g[r * nrhs + c0 + q];
+      for (int q = 0; q < 3 && c0 + q < nrhs; ++q)
+        ytile[(size_t)(r / 64) * 4096 + swz(q, (int)(r % 64))] = g[r * nrhs + c0 + q];
     H2D(dY.p, ytile.data(), sizeof(double) * ytile.size());
     H2D(dflags.p, ready.data(), sizeof(int) * ready.size());
     SPB_CUDA(cudaMemset(dcnt.p, 0, sizeof(int)));
