@@ -442,42 +442,91 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
 
 // u = L^-T y: x_j^T = (y_j^T - sum_{i>j} x_i^T L_ij) inv(L_jj). CTA b handles
 // block j = N-1-b and only waits on lower CTA indices.
+// The critical chain per block is flag -> L_{j+1,j} GEMV -> inv(L_jj) GEMV ->
+// flag, so both tiles are prefetched into shared memory at launch and the
+// post-flag work never touches global memory. The other L_ij contributions
+// are accumulated while later blocks are still being solved.
+constexpr int BW_LDS = 65;  // padded row stride of the prefetched tiles (bank-conflict free column reads)
 __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, int* __restrict__ xflags,
                                                         double* __restrict__ xrows /* N*3*64 */,
                                                         double* __restrict__ u, int m) {
-  __shared__ double xi[3 * TS];
-  __shared__ double acc_s[3 * TS];
+  extern __shared__ double bw_sm[];
+  double* sLnext = bw_sm;                 // L_{j+1,j}, plain rows (k, c) at k*BW_LDS + c
+  double* sLiT = bw_sm + TS * BW_LDS;     // LinvT_j: row c holds column c of inv(L_jj)
+  double* xi = sLiT + TS * BW_LDS;        // 3 x 64
+  double* part = xi + 3 * TS;             // 4 x 3 x 64 partial sums
   const int N = d.N;
   const int j = N - 1 - blockIdx.x;
   const int tid = threadIdx.x;
-  const int r = tid >> 6, c = tid & 63;  // r < 3 active (192 threads)
-  double acc = 0.0;
+  const int c = tid & 63, grp = tid >> 6;  // 4 groups x 64 columns
+  // prefetch (plain layout) the two tiles of the critical step
+  for (int q = tid; q < TILE; q += 256) {
+    const int k = q >> 6, cc = q & 63;
+    if (j + 1 < N) sLnext[k * BW_LDS + cc] = d.L[(size_t)tidx(j + 1, j) * TILE + swz(k, cc)];
+    sLiT[k * BW_LDS + cc] = d.LinvT[(size_t)j * TILE + swz(k, cc)];
+  }
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;  // thread (grp, c): rows k in [16 grp, 16 grp + 16)
   for (int i = N - 1; i > j; --i) {
     if (tid == 0) {
-      while (ld_relaxed(xflags + i) == 0) __nanosleep(32);
+      while (ld_relaxed(xflags + i) == 0) {
+      }
       fence_acq_rel_gpu();
     }
     __syncthreads();
     if (tid < 3 * TS) xi[tid] = __ldcg(xrows + (size_t)i * 3 * TS + tid);
     __syncthreads();
-    if (r < 3) {
+    if (i == j + 1) {
+#pragma unroll
+      for (int k = grp * 16; k < grp * 16 + 16; ++k) {
+        const double l = sLnext[k * BW_LDS + c];
+        acc0 += xi[k] * l;
+        acc1 += xi[TS + k] * l;
+        acc2 += xi[2 * TS + k] * l;
+      }
+    } else {
       const double* L = d.L + (size_t)tidx(i, j) * TILE;
-      double s = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < TS; ++k) s += xi[r * TS + k] * L[swz(k, c)];
-      acc += s;
+#pragma unroll
+      for (int k = grp * 16; k < grp * 16 + 16; ++k) {
+        const double l = L[swz(k, c)];
+        acc0 += xi[k] * l;
+        acc1 += xi[TS + k] * l;
+        acc2 += xi[2 * TS + k] * l;
+      }
     }
     __syncthreads();
   }
-  if (r < 3) acc_s[r * TS + c] = d.Y[(size_t)j * TILE + swz(r, c)] - acc;
+  part[(grp * 3 + 0) * TS + c] = acc0;
+  part[(grp * 3 + 1) * TS + c] = acc1;
+  part[(grp * 3 + 2) * TS + c] = acc2;
   __syncthreads();
-  if (r < 3) {
-    const double* LiT = d.LinvT + (size_t)j * TILE;  // x = tmp * inv(L_jj) = tmp * LinvT^T
-    double s = 0.0;
-#pragma unroll 8
-    for (int k = 0; k < TS; ++k) s += acc_s[r * TS + k] * LiT[swz(c, k)];
+  if (tid < 3 * TS) {
+    const int r = tid >> 6;
+    const double s = ((part[(0 * 3 + r) * TS + c] + part[(1 * 3 + r) * TS + c]) + part[(2 * 3 + r) * TS + c]) +
+                     part[(3 * 3 + r) * TS + c];
+    xi[tid] = d.Y[(size_t)j * TILE + swz(r, c)] - s;  // tmp = y_j - sum_i x_i L_ij
+  }
+  __syncthreads();
+  // x_j[r][c] = sum_k tmp[r][k] inv(L_jj)[k][c] = sum_k tmp[r][k] LinvT[c][k]
+  {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int k = grp * 16; k < grp * 16 + 16; ++k) {
+      const double l = sLiT[c * BW_LDS + k];
+      a0 += xi[k] * l;
+      a1 += xi[TS + k] * l;
+      a2 += xi[2 * TS + k] * l;
+    }
+    part[(grp * 3 + 0) * TS + c] = a0;
+    part[(grp * 3 + 1) * TS + c] = a1;
+    part[(grp * 3 + 2) * TS + c] = a2;
+  }
+  __syncthreads();
+  if (tid < 3 * TS) {
+    const int r = tid >> 6;
+    const double s = ((part[(0 * 3 + r) * TS + c] + part[(1 * 3 + r) * TS + c]) + part[(2 * 3 + r) * TS + c]) +
+                     part[(3 * 3 + r) * TS + c];
     xrows[(size_t)j * 3 * TS + r * TS + c] = s;
-    int row = j * TS + c;
+    const int row = j * TS + c;
     if (row < m) u[3 * row + r] = s;
   }
   __threadfence();
@@ -565,7 +614,13 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
 }
 
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, int* xflags, double* xrows, double* u) {
-  k_dense_backward<<<d.N, 256, 0, st>>>(d, xflags, xrows, u, d.m);
+  static bool attr = false;
+  const size_t smem = sizeof(double) * (2 * TS * BW_LDS + 3 * TS + 12 * TS);
+  if (!attr) {
+    cudaFuncSetAttribute(k_dense_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_dense_backward<<<d.N, 256, smem, st>>>(d, xflags, xrows, u, d.m);
 }
 
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial) {

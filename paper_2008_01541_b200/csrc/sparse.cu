@@ -9,8 +9,14 @@
 //             y_s = inv(L_ss) v_top,   U_s = v_below - W v_top
 //   backward: x_s = inv(L_ss)^T y_s - W^T x_below
 // i.e. ONE dense GEMV (3 RHS) per supernode; supernodes of the same
-// elimination-tree height run concurrently (one launch per level). The x2
-// rows of the panels are the coupling C, so the forward sweep also yields
+// elimination-tree height are independent. Each level runs as
+//   (1) a gather kernel that assembles every struct row of the level once into
+//       a contiguous buffer (forward: v = b + children's update entries;
+//       backward: z = [y_s ; -x_below]), then
+//   (2) GEMV kernels that stream the panels with coalesced loads and many
+//       independent loads in flight (CTA tasks for wide supernodes, warp tasks
+//       for nc <= 16).
+// The x2 rows of the panels are the coupling C, so the forward sweep also yields
 // f~2 = f2 - C y1 and the backward sweep consumes C^T u2 (linalg.py:395, :408).
 // Update vectors are pulled by their consumer in fixed child order: no float
 // atomics, bitwise run-to-run determinism (test_solver.py:275-283).
@@ -29,27 +35,35 @@ struct SnDev {
 
 struct LevelTasks {
   int cta_off, ncta, warp_off, nwarp;
-  int max_nc;  // forward CTA tasks: columns staged in smem
+  int pos_off, npos;  // struct positions of the level (gather kernels)
+  int max_nc;         // forward CTA tasks: columns staged in smem
 };
 
 struct DeviceFactor {
   int n1 = 0, n2 = 0, ns = 0, nlevels = 0;
   int64_t nrows_total = 0, urows = 0, nval = 0;
   SnDev* sn = nullptr;
-  int* rows = nullptr;
+  int* rows = nullptr;      // struct rows (factor positions)
+  int* pos_owner = nullptr; // per struct position: factor index of an own column (top rows) or -1
+  int* lvl_pos = nullptr;   // struct positions grouped by level
   double* M = nullptr;
+  double* VZ = nullptr;     // per struct position x 3: assembled v (forward) / z (backward)
   int* asm_ptr = nullptr;
   int* asm_src = nullptr;
   int* x2_ptr = nullptr;
   int* x2_src = nullptr;
   int2* fw_cta = nullptr;   // (s, row0)
   int2* fw_warp = nullptr;  // (s, row0)
-  int2* bw_cta = nullptr;   // (s, col0)
-  int* bw_warp = nullptr;   // s
-  std::vector<LevelTasks> fw, bw;
+  int4* bw_tiles = nullptr;   // (s, c0, r0, partial slot)
+  int4* bw_chunks = nullptr;  // (s, c0, first slot, ntiles)
+  double* P = nullptr;        // backward tile partials
+  int* bw_warp = nullptr;     // s
+  std::vector<LevelTasks> lv;
+  std::vector<int> bwt_off, bwr_off, bww_off;  // backward tile / chunk / warp offsets per level
   ~DeviceFactor() {
-    for (void* p : {(void*)sn, (void*)rows, (void*)M, (void*)asm_ptr, (void*)asm_src, (void*)x2_ptr,
-                    (void*)x2_src, (void*)fw_cta, (void*)fw_warp, (void*)bw_cta, (void*)bw_warp})
+    for (void* p : {(void*)sn, (void*)rows, (void*)pos_owner, (void*)lvl_pos, (void*)M, (void*)VZ,
+                    (void*)asm_ptr, (void*)asm_src, (void*)x2_ptr, (void*)x2_src, (void*)fw_cta, (void*)fw_warp,
+                    (void*)bw_tiles, (void*)bw_chunks, (void*)P, (void*)bw_warp})
       if (p) cudaFree(p);
   }
 };
@@ -57,52 +71,97 @@ struct DeviceFactor {
 size_t device_factor_ubuf(const DeviceFactor& df) { return (size_t)df.urows; }
 int device_factor_levels(const DeviceFactor& df) { return df.nlevels; }
 
-constexpr int FW_ROWS = 32;     // rows per forward task
-constexpr int BW_COLS = 16;     // columns per backward CTA task
-constexpr int WARP_NC = 32;     // supernodes with nc <= this use warp tasks
+constexpr int FW_ROWS = 32;     // rows per forward CTA task (16 column groups x 32 rows)
+constexpr int FW_THREADS = 512;
+constexpr int FW_WARPS = FW_THREADS / 32;
+constexpr int BT_ROWS = 512;       // backward tile rows
+constexpr int BT_COLS = 32;        // backward tile columns (8 warps x 4)
+constexpr int BW_WARP_MAXNR = 128; // small supernodes with longer columns take the tile path
+constexpr int FW_WROWS = 32;    // rows per forward warp task
+constexpr int WARP_NC = 16;     // supernodes with nc <= this use warp tasks
 constexpr int CH_FW = 4096;     // forward column chunk staged in smem
-constexpr int CH_BW = 4096;     // backward row chunk staged in smem
 
-// -------------------------------------------------------------- forward
-__device__ __forceinline__ double asm_sum(const int* __restrict__ ap, const int* __restrict__ as,
-                                          const double* __restrict__ U, int64_t p, int q, double init) {
-  double v = init;
-  for (int k = ap[p]; k < ap[p + 1]; ++k) v += U[3 * (int64_t)as[k] + q];
-  return v;
+// ------------------------------------------------------------- gathers
+// forward: V[p] = b[own column] (top rows) + sum of the children's update
+// entries landing on struct position p, in fixed child order.
+__global__ void k_fw_gather(const int* __restrict__ lvl_pos, int npos, const int* __restrict__ owner,
+                            const int* __restrict__ ap, const int* __restrict__ as, const double* __restrict__ U,
+                            const double* __restrict__ b, double* __restrict__ V) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npos) return;
+  const int p = lvl_pos[t];
+  const int o = owner[p];
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  if (o >= 0) {
+    v0 = b[3 * (int64_t)o + 0];
+    v1 = b[3 * (int64_t)o + 1];
+    v2 = b[3 * (int64_t)o + 2];
+  }
+  for (int k = ap[p]; k < ap[p + 1]; ++k) {
+    const double* u = U + 3 * (int64_t)as[k];
+    v0 += u[0];
+    v1 += u[1];
+    v2 += u[2];
+  }
+  V[3 * (int64_t)p + 0] = v0;
+  V[3 * (int64_t)p + 1] = v1;
+  V[3 * (int64_t)p + 2] = v2;
 }
 
-__global__ void __launch_bounds__(256) k_forward_level(const SnDev* __restrict__ sn, const double* __restrict__ M,
-                                                       const int* __restrict__ ap, const int* __restrict__ as,
+// backward: Z[p] = y[own column] for top rows, -x[row] below (x2 rows hold u2_accum)
+__global__ void k_bw_gather(const int* __restrict__ lvl_pos, int npos, const int* __restrict__ owner,
+                            const int* __restrict__ rows, const double* __restrict__ y,
+                            const double* __restrict__ XF, double* __restrict__ Z) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= npos) return;
+  const int p = lvl_pos[t];
+  const int o = owner[p];
+  double z0, z1, z2;
+  if (o >= 0) {
+    z0 = y[3 * (int64_t)o + 0];
+    z1 = y[3 * (int64_t)o + 1];
+    z2 = y[3 * (int64_t)o + 2];
+  } else {
+    const double* x = XF + 3 * (int64_t)rows[p];
+    z0 = -x[0];
+    z1 = -x[1];
+    z2 = -x[2];
+  }
+  Z[3 * (int64_t)p + 0] = z0;
+  Z[3 * (int64_t)p + 1] = z1;
+  Z[3 * (int64_t)p + 2] = z2;
+}
+
+// -------------------------------------------------------------- forward
+// CTA task (s, r0): rows r0..r0+31 of M_s; warp w walks columns w, w+8, ...
+// (8 independent loads in flight per lane); partials summed in fixed order.
+// Warp task (s, r0): one lane per row, the <= 16 inputs broadcast by shuffles.
+__global__ void __launch_bounds__(FW_THREADS) k_forward_level(const SnDev* __restrict__ sn, const double* __restrict__ M,
+                                                       const double* __restrict__ V,
                                                        const int2* __restrict__ cta_tasks, int ncta,
                                                        const int2* __restrict__ warp_tasks, int nwarp,
-                                                       const double* __restrict__ b, double* __restrict__ y,
-                                                       double* __restrict__ U) {
+                                                       double* __restrict__ y, double* __restrict__ U) {
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if ((int)blockIdx.x < ncta) {
-    // ---------------- CTA task: 32 rows, columns split over 8 warps
     const int2 tk = cta_tasks[blockIdx.x];
     const SnDev S = sn[tk.x];
     const int r = tk.y + lane;
     const bool valid = r < S.nr;
     const int cmax = (tk.y < S.nc) ? min(S.nc, tk.y + FW_ROWS) : S.nc;
+    const double* Vs = V + 3 * (int64_t)S.rowoff;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    const double* Mp = M + S.valoff + r;
+    const double* Mp = M + S.valoff + (valid ? r : 0);
     for (int c0 = 0; c0 < cmax; c0 += CH_FW) {
       const int c1 = min(cmax, c0 + CH_FW);
       __syncthreads();
-      for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-        int64_t p = (int64_t)S.rowoff + c;
-        int gi = S.first + c;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) sm[3 * (c - c0) + q] = asm_sum(ap, as, U, p, q, b[3 * (int64_t)gi + q]);
-      }
+      for (int q = threadIdx.x; q < 3 * (c1 - c0); q += blockDim.x) sm[q] = Vs[3 * c0 + q];
       __syncthreads();
       if (valid) {
         int c = c0 + warp;
-#pragma unroll 4
-        for (; c < c1; c += 8) {
-          double mv = Mp[(int64_t)c * S.nr];
+#pragma unroll 16
+        for (; c < c1; c += FW_WARPS) {
+          const double mv = Mp[(int64_t)c * S.nr];
           const double* v = sm + 3 * (c - c0);
           a0 += mv * v[0];
           a1 += mv * v[1];
@@ -111,7 +170,7 @@ __global__ void __launch_bounds__(256) k_forward_level(const SnDev* __restrict__
       }
     }
     __syncthreads();
-    double* red = sm;  // [8][32][3]
+    double* red = sm;  // [FW_WARPS][32][3]
     red[(warp * 32 + lane) * 3 + 0] = a0;
     red[(warp * 32 + lane) * 3 + 1] = a1;
     red[(warp * 32 + lane) * 3 + 2] = a2;
@@ -122,38 +181,35 @@ __global__ void __launch_bounds__(256) k_forward_level(const SnDev* __restrict__
       if (rr < S.nr) {
         double s = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) s += red[(w * 32 + rl) * 3 + q];
-        if (rr < S.nc) {
-          y[3 * (int64_t)(S.first + rr) + q] = s;
-        } else {
-          double vb = asm_sum(ap, as, U, (int64_t)S.rowoff + rr, q, 0.0);
-          U[3 * (int64_t)(S.uoff + rr - S.nc) + q] = vb - s;
-        }
+        for (int w = 0; w < FW_WARPS; ++w) s += red[(w * 32 + rl) * 3 + q];
+        if (rr < S.nc) y[3 * (int64_t)(S.first + rr) + q] = s;
+        else U[3 * (int64_t)(S.uoff + rr - S.nc) + q] = Vs[3 * rr + q] - s;
       }
     }
   } else {
-    // ---------------- warp task: whole small panel row block in one warp
-    const int t = ((int)blockIdx.x - ncta) * 8 + warp;
+    const int t = ((int)blockIdx.x - ncta) * FW_WARPS + warp;
     if (t >= nwarp) return;
     const int2 tk = warp_tasks[t];
     const SnDev S = sn[tk.x];
+    const double* Vs = V + 3 * (int64_t)S.rowoff;
     double v0 = 0.0, v1 = 0.0, v2 = 0.0;
     if (lane < S.nc) {
-      int64_t p = (int64_t)S.rowoff + lane;
-      int gi = S.first + lane;
-      v0 = asm_sum(ap, as, U, p, 0, b[3 * (int64_t)gi + 0]);
-      v1 = asm_sum(ap, as, U, p, 1, b[3 * (int64_t)gi + 1]);
-      v2 = asm_sum(ap, as, U, p, 2, b[3 * (int64_t)gi + 2]);
+      v0 = Vs[3 * lane + 0];
+      v1 = Vs[3 * lane + 1];
+      v2 = Vs[3 * lane + 2];
     }
     const int r = tk.y + lane;
     const bool valid = r < S.nr;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     const double* Mp = M + S.valoff + (valid ? r : 0);
-    for (int c = 0; c < S.nc; ++c) {
-      double mv = valid ? Mp[(int64_t)c * S.nr] : 0.0;
-      a0 += mv * __shfl_sync(0xffffffffu, v0, c);
-      a1 += mv * __shfl_sync(0xffffffffu, v1, c);
-      a2 += mv * __shfl_sync(0xffffffffu, v2, c);
+#pragma unroll
+    for (int c = 0; c < WARP_NC; ++c) {
+      if (c < S.nc) {
+        const double mv = valid ? Mp[(int64_t)c * S.nr] : 0.0;
+        a0 += mv * __shfl_sync(0xffffffffu, v0, c);
+        a1 += mv * __shfl_sync(0xffffffffu, v1, c);
+        a2 += mv * __shfl_sync(0xffffffffu, v2, c);
+      }
     }
     if (valid) {
       if (r < S.nc) {
@@ -161,11 +217,10 @@ __global__ void __launch_bounds__(256) k_forward_level(const SnDev* __restrict__
         y[3 * (int64_t)(S.first + r) + 1] = a1;
         y[3 * (int64_t)(S.first + r) + 2] = a2;
       } else {
-        int64_t p = (int64_t)S.rowoff + r;
-        int64_t o = 3 * (int64_t)(S.uoff + r - S.nc);
-        U[o + 0] = asm_sum(ap, as, U, p, 0, 0.0) - a0;
-        U[o + 1] = asm_sum(ap, as, U, p, 1, 0.0) - a1;
-        U[o + 2] = asm_sum(ap, as, U, p, 2, 0.0) - a2;
+        const int64_t o = 3 * (int64_t)(S.uoff + r - S.nc);
+        U[o + 0] = Vs[3 * r + 0] - a0;
+        U[o + 1] = Vs[3 * r + 1] - a1;
+        U[o + 2] = Vs[3 * r + 2] - a2;
       }
     }
   }
@@ -183,92 +238,117 @@ __global__ void k_forward_x2(int n1, int n2, const int* __restrict__ xp, const i
 }
 
 // ------------------------------------------------------------- backward
-// XF: (n,3) with rows [0,n1) = x1 solution (being produced), [n1,n) = x2 input.
-__global__ void __launch_bounds__(256) k_backward_level(const SnDev* __restrict__ sn, const double* __restrict__ M,
-                                                        const int* __restrict__ rows,
-                                                        const int2* __restrict__ cta_tasks, int ncta,
-                                                        const int* __restrict__ warp_tasks, int nwarp,
-                                                        const double* __restrict__ y, double* __restrict__ XF) {
-  extern __shared__ __align__(16) double sm[];
+// Sum v[0..16) over the 32 lanes so that lane l ends with the total of entry
+// l % 16 (all-to-all butterfly: 31 shuffles instead of 16 x 5).
+__device__ __forceinline__ double warp_transpose_sum16(double (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = upper ? v[i] : v[i + off];
+      const double keep = upper ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+// Backward 2D tiles: tile (s, c0, r0) covers rows [r0, r0+BT_ROWS) x columns
+// [c0, c0+32) of M_s. The z chunk is staged in smem once per tile; warp w owns
+// 4 columns, lanes walk rows (coalesced), 16 panel loads in flight per lane.
+// Per-tile partial sums go to P[slot]; k_bw_reduce adds the row-chunk partials
+// of every column in fixed order (deterministic, no atomics).
+__global__ void __launch_bounds__(256) k_bw_tile(const SnDev* __restrict__ sn, const double* __restrict__ M,
+                                                 const double* __restrict__ Z, const int4* __restrict__ tiles,
+                                                 double* __restrict__ P) {
+  __shared__ double zs[3 * BT_ROWS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if ((int)blockIdx.x < ncta) {
-    const int2 tk = cta_tasks[blockIdx.x];
-    const SnDev S = sn[tk.x];
-    const int* rw = rows + S.rowoff;
-    double acc[2][3] = {{0, 0, 0}, {0, 0, 0}};
-    const int cA = tk.y + warp * 2;
-    // rows < c never contribute to column c (inv(L_ss) is lower triangular)
-    const int rstart = tk.y;
-    for (int r0 = rstart; r0 < S.nr; r0 += CH_BW) {
-      const int r1 = min(S.nr, r0 + CH_BW);
-      __syncthreads();
-      for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-        if (r < S.nc) {
+  const int4 tk = tiles[blockIdx.x];  // (s, c0, r0, slot)
+  const SnDev S = sn[tk.x];
+  const int c0 = tk.y, r0 = tk.z;
+  const int nrt = min(BT_ROWS, S.nr - r0);
+  const double* Zs = Z + 3 * ((int64_t)S.rowoff + r0);
+  for (int q = threadIdx.x; q < 3 * nrt; q += 256) zs[q] = Zs[q];
+  __syncthreads();
+  double acc[4][3];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) sm[3 * (r - r0) + q] = y[3 * (int64_t)(S.first + r) + q];
-        } else {
-          const int64_t g = rw[r];
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.0;
+  const int cb = c0 + 4 * warp;
+  const double* Mt = M + S.valoff + (int64_t)cb * S.nr + r0;
+  const int nci = max(0, min(4, S.nc - cb));
+  if (nci > 0) {
+#pragma unroll 4
+    for (int k = lane; k < nrt; k += 32) {
+      const double z0 = zs[3 * k], z1 = zs[3 * k + 1], z2 = zs[3 * k + 2];
 #pragma unroll
-          for (int q = 0; q < 3; ++q) sm[3 * (r - r0) + q] = -XF[3 * g + q];
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = cA + cc;
-        if (c >= S.nc) continue;
-        const double* Mc = M + S.valoff + (int64_t)c * S.nr;
-        for (int r = max(r0, c) + lane; r < r1; r += 32) {
-          double mv = Mc[r];
-          const double* z = sm + 3 * (r - r0);
-          acc[cc][0] += mv * z[0];
-          acc[cc][1] += mv * z[1];
-          acc[cc][2] += mv * z[2];
+      for (int i = 0; i < 4; ++i) {
+        if (i < nci) {
+          const double m = Mt[(int64_t)i * S.nr + k];
+          acc[i][0] += m * z0;
+          acc[i][1] += m * z1;
+          acc[i][2] += m * z2;
         }
       }
     }
+  }
+  double* out = P + (int64_t)tk.w * (BT_COLS * 3);
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int c = cA + cc;
-      double s0 = warp_sum(acc[cc][0]), s1 = warp_sum(acc[cc][1]), s2 = warp_sum(acc[cc][2]);
-      if (lane == 0 && c < S.nc) {
-        XF[3 * (int64_t)(S.first + c) + 0] = s0;
-        XF[3 * (int64_t)(S.first + c) + 1] = s1;
-        XF[3 * (int64_t)(S.first + c) + 2] = s2;
-      }
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double v = warp_sum(acc[i][q]);
+      if (lane == 0) out[(4 * warp + i) * 3 + q] = v;
     }
-  } else {
-    const int t = ((int)blockIdx.x - ncta) * 8 + warp;
-    if (t >= nwarp) return;
-    const SnDev S = sn[warp_tasks[t]];
-    const int* rw = rows + S.rowoff;
-    const int c = lane;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    const double* Mc = M + S.valoff + (int64_t)(c < S.nc ? c : 0) * S.nr;
-    for (int r = 0; r < S.nr; ++r) {
-      double z0, z1, z2;
-      if (r < S.nc) {
-        z0 = y[3 * (int64_t)(S.first + r) + 0];
-        z1 = y[3 * (int64_t)(S.first + r) + 1];
-        z2 = y[3 * (int64_t)(S.first + r) + 2];
-      } else {
-        const int64_t g = rw[r];
-        z0 = -XF[3 * g + 0];
-        z1 = -XF[3 * g + 1];
-        z2 = -XF[3 * g + 2];
-      }
-      if (c < S.nc && r >= c) {
-        double mv = Mc[r];
-        a0 += mv * z0;
-        a1 += mv * z1;
-        a2 += mv * z2;
-      }
+}
+
+// x[first + c0 + cc] = sum over the chunk's row tiles (ascending r0) of P.
+__global__ void k_bw_reduce(const SnDev* __restrict__ sn, const int4* __restrict__ chunks, int nchunks,
+                            const double* __restrict__ P, double* __restrict__ XF) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nchunks * BT_COLS * 3) return;
+  const int ch = t / (BT_COLS * 3), e = t % (BT_COLS * 3);
+  const int cc = e / 3, q = e % 3;
+  const int4 c = chunks[ch];  // (s, c0, first slot, ntiles)
+  const SnDev S = sn[c.x];
+  if (c.y + cc >= S.nc) return;
+  double s = 0.0;
+  for (int k = 0; k < c.w; ++k) s += P[((int64_t)(c.z + k) * BT_COLS + cc) * 3 + q];
+  XF[3 * (int64_t)(S.first + c.y + cc) + q] = s;
+}
+
+// Warp task (s), nc <= 16: lanes over rows, one RHS at a time (low register
+// footprint for occupancy), then the butterfly.
+__global__ void __launch_bounds__(256) k_backward_warp(const SnDev* __restrict__ sn, const double* __restrict__ M,
+                                                       const double* __restrict__ Z,
+                                                       const int* __restrict__ warp_tasks, int nwarp,
+                                                       double* __restrict__ XF) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= nwarp) return;
+  const SnDev S = sn[warp_tasks[t]];
+  const double* Zs = Z + 3 * (int64_t)S.rowoff;
+  const double* Mc = M + S.valoff;
+  double out[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    double acc[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
+    for (int r = lane; r < S.nr; r += 32) {
+      const double z = Zs[3 * r + q];
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc)
+        if (cc < S.nc) acc[cc] += Mc[(int64_t)cc * S.nr + r] * z;
     }
-    if (c < S.nc) {
-      XF[3 * (int64_t)(S.first + c) + 0] = a0;
-      XF[3 * (int64_t)(S.first + c) + 1] = a1;
-      XF[3 * (int64_t)(S.first + c) + 2] = a2;
-    }
+    out[q] = warp_transpose_sum16(acc, lane);
+  }
+  if (lane < S.nc) {
+    XF[3 * (int64_t)(S.first + lane) + 0] = out[0];
+    XF[3 * (int64_t)(S.first + lane) + 1] = out[1];
+    XF[3 * (int64_t)(S.first + lane) + 2] = out[2];
   }
 }
 
@@ -291,7 +371,11 @@ int build_device_factor(Factor& f) {
   d->nlevels = (int)f.nlevels;
   d->nrows_total = f.sn_rowptr.empty() ? 0 : f.sn_rowptr[ns];
   d->nval = f.sn_valptr.empty() ? 0 : f.sn_valptr[ns];
-  if (d->nrows_total >= (int64_t)1 << 31) { delete d; set_error("factor too large (row index > 2^31)"); return SPB_ERR_SETUP; }
+  if (d->nrows_total >= (int64_t)1 << 31) {
+    delete d;
+    set_error("factor too large (row index > 2^31)");
+    return SPB_ERR_SETUP;
+  }
   std::vector<SnDev> sn(ns);
   int64_t uoff = 0;
   for (int64_t s = 0; s < ns; ++s) {
@@ -306,8 +390,10 @@ int build_device_factor(Factor& f) {
     uoff += S.nr - S.nc;
   }
   d->urows = uoff;
-  std::vector<int> rows(d->nrows_total);
+  std::vector<int> rows(d->nrows_total), owner(d->nrows_total, -1);
   for (int64_t k = 0; k < d->nrows_total; ++k) rows[k] = (int)f.sn_rows[k];
+  for (int64_t s = 0; s < ns; ++s)
+    for (int k = 0; k < sn[s].nc; ++k) owner[sn[s].rowoff + k] = sn[s].first + k;
   // forward extend-add maps (children in ascending order)
   std::vector<std::vector<int64_t>> children(ns);
   for (int64_t s = 0; s < ns; ++s)
@@ -335,7 +421,8 @@ int build_device_factor(Factor& f) {
     }
   };
   for_each_map([&](bool x2, int64_t p, int) {
-    if (x2) xcnt[p + 1]++; else cnt[p + 1]++;
+    if (x2) xcnt[p + 1]++;
+    else cnt[p + 1]++;
   });
   for (int64_t k = 0; k < d->nrows_total; ++k) cnt[k + 1] += cnt[k];
   for (int64_t k = 0; k < f.n2; ++k) xcnt[k + 1] += xcnt[k];
@@ -343,53 +430,79 @@ int build_device_factor(Factor& f) {
   {
     std::vector<int> fill(cnt.begin(), cnt.end() - 1), xfill(xcnt.begin(), xcnt.end() - 1);
     for_each_map([&](bool x2, int64_t p, int src) {
-      if (x2) xsrc[xfill[p]++] = src; else asrc[fill[p]++] = src;
+      if (x2) xsrc[xfill[p]++] = src;
+      else asrc[fill[p]++] = src;
     });
   }
-  // level task lists
+  // per level: forward tasks, backward tasks, struct positions
   std::vector<std::vector<int64_t>> bylevel(f.nlevels);
   for (int64_t s = 0; s < ns; ++s) bylevel[f.sn_level[s]].push_back(s);
-  std::vector<int2> fwc, fww, bwc;
-  std::vector<int> bww;
-  d->fw.resize(f.nlevels);
-  d->bw.resize(f.nlevels);
+  std::vector<int2> fwc, fww;
+  std::vector<int4> bwt, bwr;
+  std::vector<int> bww, lpos;
+  lpos.reserve(d->nrows_total);
+  d->lv.resize(f.nlevels);
+  d->bwt_off.assign(f.nlevels + 1, 0);
+  d->bwr_off.assign(f.nlevels + 1, 0);
+  d->bww_off.assign(f.nlevels + 1, 0);
   for (int64_t l = 0; l < f.nlevels; ++l) {
-    LevelTasks& F = d->fw[l];
-    LevelTasks& B = d->bw[l];
-    F.cta_off = (int)fwc.size();
-    F.warp_off = (int)fww.size();
-    B.cta_off = (int)bwc.size();
-    B.warp_off = (int)bww.size();
-    F.max_nc = 0;
+    LevelTasks& T = d->lv[l];
+    T.cta_off = (int)fwc.size();
+    T.warp_off = (int)fww.size();
+    T.pos_off = (int)lpos.size();
+    T.max_nc = 0;
+    d->bwt_off[l] = (int)bwt.size();
+    d->bwr_off[l] = (int)bwr.size();
+    d->bww_off[l] = (int)bww.size();
     for (int64_t s : bylevel[l]) {
       const SnDev& S = sn[s];
-      bool small = S.nc <= WARP_NC;
-      for (int r0 = 0; r0 < S.nr; r0 += FW_ROWS) {
-        if (small) fww.push_back(make_int2((int)s, r0));
-        else fwc.push_back(make_int2((int)s, r0));
+      const bool small = S.nc <= WARP_NC;
+      if (small) {
+        for (int r0 = 0; r0 < S.nr; r0 += FW_WROWS) fww.push_back(make_int2((int)s, r0));
+      } else {
+        for (int r0 = 0; r0 < S.nr; r0 += FW_ROWS) fwc.push_back(make_int2((int)s, r0));
+        T.max_nc = std::max(T.max_nc, S.nc);
       }
-      if (!small) F.max_nc = std::max(F.max_nc, S.nc);
-      if (small) bww.push_back((int)s);
-      else
-        for (int c0 = 0; c0 < S.nc; c0 += BW_COLS) bwc.push_back(make_int2((int)s, c0));
+      if (small && S.nr <= BW_WARP_MAXNR) {
+        bww.push_back((int)s);
+      } else {
+        for (int c0 = 0; c0 < S.nc; c0 += BT_COLS) {
+          const int slot0 = (int)bwt.size();
+          for (int r0 = 0; r0 < S.nr; r0 += BT_ROWS) {
+            if (r0 + BT_ROWS <= c0) continue;  // entirely above the diagonal of inv(L_ss): zero
+            bwt.push_back(make_int4((int)s, c0, r0, (int)bwt.size()));
+          }
+          bwr.push_back(make_int4((int)s, c0, slot0, (int)bwt.size() - slot0));
+        }
+      }
+      for (int k = 0; k < S.nr; ++k) lpos.push_back(S.rowoff + k);
     }
-    F.ncta = (int)fwc.size() - F.cta_off;
-    F.nwarp = (int)fww.size() - F.warp_off;
-    B.ncta = (int)bwc.size() - B.cta_off;
-    B.nwarp = (int)bww.size() - B.warp_off;
+    T.ncta = (int)fwc.size() - T.cta_off;
+    T.nwarp = (int)fww.size() - T.warp_off;
+    T.npos = (int)lpos.size() - T.pos_off;
   }
+  d->bwt_off[f.nlevels] = (int)bwt.size();
+  d->bwr_off[f.nlevels] = (int)bwr.size();
+  d->bww_off[f.nlevels] = (int)bww.size();
   int rc;
-  if ((rc = upload(&d->sn, sn)) || (rc = upload(&d->rows, rows)) || (rc = upload(&d->M, f.Mval)) ||
-      (rc = upload(&d->asm_ptr, cnt)) || (rc = upload(&d->asm_src, asrc)) || (rc = upload(&d->x2_ptr, xcnt)) ||
-      (rc = upload(&d->x2_src, xsrc)) || (rc = upload(&d->fw_cta, fwc)) || (rc = upload(&d->fw_warp, fww)) ||
-      (rc = upload(&d->bw_cta, bwc)) || (rc = upload(&d->bw_warp, bww))) {
+  if ((rc = upload(&d->sn, sn)) || (rc = upload(&d->rows, rows)) || (rc = upload(&d->pos_owner, owner)) ||
+      (rc = upload(&d->lvl_pos, lpos)) || (rc = upload(&d->M, f.Mval)) || (rc = upload(&d->asm_ptr, cnt)) ||
+      (rc = upload(&d->asm_src, asrc)) || (rc = upload(&d->x2_ptr, xcnt)) || (rc = upload(&d->x2_src, xsrc)) ||
+      (rc = upload(&d->fw_cta, fwc)) || (rc = upload(&d->fw_warp, fww)) || (rc = upload(&d->bw_tiles, bwt)) ||
+      (rc = upload(&d->bw_chunks, bwr)) ||
+      (rc = upload(&d->bw_warp, bww))) {
     delete d;
     return rc;
+  }
+  if (cudaMalloc(&d->VZ, sizeof(double) * 3 * std::max<int64_t>(d->nrows_total, 1)) != cudaSuccess ||
+      cudaMalloc(&d->P, sizeof(double) * 3 * BT_COLS * std::max<size_t>(bwt.size(), 1)) != cudaSuccess) {
+    delete d;
+    set_error("cudaMalloc failed (sweep buffer)");
+    return SPB_ERR_CUDA;
   }
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_forward_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
-    cudaFuncSetAttribute(k_backward_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_BW * 8 + 64);
     attr = true;
   }
   f.dev = d;
@@ -399,13 +512,16 @@ int build_device_factor(Factor& f) {
 void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
                     int* launches) {
   for (int l = 0; l < d.nlevels; ++l) {
-    const LevelTasks& T = d.fw[l];
-    int grid = T.ncta + (T.nwarp + 7) / 8;
-    if (grid == 0) continue;
-    size_t smem = T.ncta ? std::max<size_t>(sizeof(double) * 3 * std::min(T.max_nc, CH_FW), 8 * 32 * 3 * 8) : 0;
-    k_forward_level<<<grid, 256, smem, st>>>(d.sn, d.M, d.asm_ptr, d.asm_src, d.fw_cta + T.cta_off, T.ncta,
-                                             d.fw_warp + T.warp_off, T.nwarp, b, y, U);
-    if (launches) ++*launches;
+    const LevelTasks& T = d.lv[l];
+    if (T.npos == 0) continue;
+    k_fw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.asm_ptr,
+                                                       d.asm_src, U, b, d.VZ);
+    const int grid = T.ncta + (T.nwarp + FW_WARPS - 1) / FW_WARPS;
+    const size_t smem =
+        T.ncta ? std::max<size_t>(sizeof(double) * 3 * std::min(T.max_nc, CH_FW), FW_WARPS * 32 * 3 * 8) : 0;
+    k_forward_level<<<grid, FW_THREADS, smem, st>>>(d.sn, d.M, d.VZ, d.fw_cta + T.cta_off, T.ncta, d.fw_warp + T.warp_off,
+                                             T.nwarp, y, U);
+    if (launches) *launches += 2;
   }
   if (d.n2 > 0) {
     k_forward_x2<<<ceil_div(3 * (int64_t)d.n2, 256), 256, 0, st>>>(d.n1, d.n2, d.x2_ptr, d.x2_src, U, b, f2);
@@ -415,13 +531,20 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
 
 void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches) {
   for (int l = d.nlevels - 1; l >= 0; --l) {
-    const LevelTasks& T = d.bw[l];
-    int grid = T.ncta + (T.nwarp + 7) / 8;
-    if (grid == 0) continue;
-    size_t smem = T.ncta ? sizeof(double) * 3 * CH_BW : 0;
-    k_backward_level<<<grid, 256, smem, st>>>(d.sn, d.M, d.rows, d.bw_cta + T.cta_off, T.ncta,
-                                              d.bw_warp + T.warp_off, T.nwarp, y, XF);
-    if (launches) ++*launches;
+    const LevelTasks& T = d.lv[l];
+    if (T.npos == 0) continue;
+    k_bw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.rows, y, XF,
+                                                       d.VZ);
+    const int nt = d.bwt_off[l + 1] - d.bwt_off[l];
+    const int nr = d.bwr_off[l + 1] - d.bwr_off[l];
+    const int nw = d.bww_off[l + 1] - d.bww_off[l];
+    if (nt) {
+      k_bw_tile<<<nt, 256, 0, st>>>(d.sn, d.M, d.VZ, d.bw_tiles + d.bwt_off[l], d.P);
+      k_bw_reduce<<<ceil_div((int64_t)nr * BT_COLS * 3, 256), 256, 0, st>>>(d.sn, d.bw_chunks + d.bwr_off[l], nr, d.P,
+                                                                            XF);
+    }
+    if (nw) k_backward_warp<<<(nw + 7) / 8, 256, 0, st>>>(d.sn, d.M, d.VZ, d.bw_warp + d.bww_off[l], nw, XF);
+    if (launches) *launches += 1 + 2 * (nt > 0) + (nw > 0);
   }
 }
 
