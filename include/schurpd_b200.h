@@ -187,6 +187,8 @@ int32_t spb_ctx_get_state(spb_ctx *ctx, double *x, double *R, double *Q, uint8_t
  * resident in HBM; reports the mean device ms per frame (CUDA events). */
 int32_t spb_ctx_bench(spb_ctx *ctx, const spb_step_config *cfg, int32_t frames, double *ms_per_frame,
                       double *phase_ms /* [6]: local, forward, inner-detect, dense, backward, metrics */);
+/* Diagnostics: per-task timestamps of one tile-Cholesky launch (see context.cu). */
+int32_t spb_ctx_trace_cholesky(spb_ctx *ctx, uint64_t *out, int32_t *tasks_out, int32_t *ntasks);
 /* Cholesky-only timing on the context's current H (tile kernel), ms per launch. */
 int32_t spb_ctx_bench_cholesky(spb_ctx *ctx, int32_t reps, double *ms);
 

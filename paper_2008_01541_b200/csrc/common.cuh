@@ -77,7 +77,9 @@ inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) 
 // Dense 64x64 FP64 tiles are stored "swizzled row-major": element (r, c) at
 // r*64 + (c ^ ((r & 3) << 2)). The XOR moves 4-column groups so that DMMA
 // fragment loads (8 rows x 4 consecutive k) hit 16 distinct 8-byte bank slots
-// per half-warp, while whole tiles stay contiguous for 1D bulk (TMA) copies.
+// per half-warp, while whole tiles stay contiguous for one 32 KB bulk (TMA)
+// copy. The XOR only touches column bits 2-3, which are lane constants in the
+// fragment loads, so those keep register + immediate addressing.
 __host__ __device__ __forceinline__ int swz(int r, int c) { return r * 64 + (c ^ ((r & 3) << 2)); }
 
 __device__ __forceinline__ int ld_relaxed(const int* p) {

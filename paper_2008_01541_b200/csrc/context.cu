@@ -686,6 +686,30 @@ int32_t spb_ctx_bench(spb_ctx* cp, const spb_step_config* cfg, int32_t frames, d
   SPB_GUARD_END
 }
 
+// Diagnostics: one traced Cholesky launch; out = 4 x ntasks u64
+// {claim ns, k-loop done ns, finalize done ns, sm id} in task-list order,
+// plus the task list itself (i, j) in tasks_out (2 x ntasks int32).
+int32_t spb_ctx_trace_cholesky(spb_ctx* cp, uint64_t* out, int32_t* tasks_out, int32_t* ntasks) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  *ntasks = c->ntasks;
+  if (!out) return SPB_OK;
+  SPB_CUDA(cudaSetDevice(c->device));
+  unsigned long long* tr = nullptr;
+  SPB_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * 4 * c->ntasks));
+  spb::DenseDev dd = c->dd;
+  dd.trace = tr;
+  SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
+  SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
+  spb::launch_cholesky_tiles(c->st, dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  SPB_CUDA(cudaMemcpy(out, tr, sizeof(unsigned long long) * 4 * c->ntasks, cudaMemcpyDeviceToHost));
+  SPB_CUDA(cudaMemcpy(tasks_out, c->tasks.p, sizeof(int2) * c->ntasks, cudaMemcpyDeviceToHost));
+  cudaFree(tr);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
 int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);

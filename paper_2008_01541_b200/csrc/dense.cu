@@ -27,28 +27,34 @@
 namespace spb {
 
 constexpr int TS = 64;
-constexpr int TILE = TS * TS;            // doubles per tile
+constexpr int TILE = TS * TS;            // doubles per tile (global, row-major)
 constexpr int TILE_BYTES = TILE * 8;     // 32 KB
+constexpr int PTILE = TILE;              // doubles per smem stage tile (swizzled, unpadded)
 constexpr int NSTAGE = 3;
 constexpr int NCONS = 256;               // consumer threads (8 warps)
 constexpr int NTHREADS = NCONS + 32;     // + 1 producer warp
 constexpr int LDP = 66;                  // plain row stride of the potrf scratch
-#ifndef SPB_CHOL_CPASYNC
-#define SPB_CHOL_CPASYNC 0               // 1: generic-proxy cp.async producer instead of bulk TMA
-#endif
 
 __host__ __device__ __forceinline__ int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
 int dense_tile_count(int N) { return N * (N + 1) / 2; }
 
+// dynamic smem: [stage s][slot a/b] padded tiles, then col[2][128], ipiv[2],
+// then the mbarriers and the task slot
+constexpr int SM_STAGES = NSTAGE * 2 * PTILE;
+constexpr int SM_COL = SM_STAGES;
+constexpr int SM_IPIV = SM_COL + 2 * 128;
+constexpr int SM_BAR = SM_IPIV + 2;  // in doubles (8-byte aligned)
+size_t cholesky_smem_bytes() { return sizeof(double) * (SM_BAR + 2 * NSTAGE + 1); }
+
 struct CholSmem {
-  double stage[NSTAGE][2][TILE];
-  double col[2][128];
-  double ipiv[2];
-  unsigned long long full[NSTAGE];
-  unsigned long long empty[NSTAGE];
-  int task;
+  double* stage0;
+  double* col;                // [2][128]
+  double* ipiv;               // [2]
+  unsigned long long* full;   // [NSTAGE]
+  unsigned long long* empty;  // [NSTAGE]
+  int* task;
+  __device__ __forceinline__ double* slot(int s, int k) const { return stage0 + (s * 2 + k) * PTILE; }
 };
-size_t cholesky_smem_bytes() { return sizeof(CholSmem) + 128; }
 
 // ------------------------------------------------------------- primitives
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -80,11 +86,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, int bytes, 
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCONS) : "memory"); }
 
 // Spin (one thread) until a readiness flag is set, then order later reads
@@ -108,45 +116,67 @@ __device__ __forceinline__ void acc_zero(Acc& a) {
     for (int nb = 0; nb < 2; ++nb) a.c[mb][nb][0] = a.c[mb][nb][1] = 0.0;
 }
 
-// acc (+/-)= A * B^T, A and B swizzled 64x64 (rows of B are the n index).
+// acc (+/-)= A * B^T over K = 64, A and B swizzled smem tiles (rows of B are
+// the n index). Lane (g, t) reads logical column 16a + 4b + t of rows with
+// (row & 3) = g & 3, i.e. physical column 16a + 4(b ^ (g & 3)) + t: four
+// per-lane base offsets (one per b) plus immediates.
 template <bool NEG>
 __device__ __forceinline__ void mma_abt(Acc& acc, const double* sA, const double* sB, int wr, int wc, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll 4
-  for (int kk = 0; kk < TS; kk += 4) {
-    double a[4], b[2];
+  const int g = lane >> 2, t = lane & 3, gq = g & 3;
+  const double* pa = sA + (wr * 32 + g) * TS + t;
+  const double* pb = sB + (wc * 16 + g) * TS + t;
+  int ob[4];
 #pragma unroll
-    for (int mb = 0; mb < 4; ++mb) {
-      double v = sA[swz(wr * 32 + mb * 8 + g, kk + t)];
-      a[mb] = NEG ? -v : v;
+  for (int b = 0; b < 4; ++b) ob[b] = 4 * (b ^ gq);
+#pragma unroll
+  for (int a16 = 0; a16 < TS; a16 += 16) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double av[4], bv[2];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        const double v = pa[ob[b] + mb * 8 * TS + a16];
+        av[mb] = NEG ? -v : v;
+      }
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) bv[nb] = pb[ob[b] + nb * 8 * TS + a16];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], av[mb], bv[nb]);
     }
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) b[nb] = sB[swz(wc * 16 + nb * 8 + g, kk + t)];
-#pragma unroll
-    for (int mb = 0; mb < 4; ++mb)
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], a[mb], b[nb]);
   }
 }
 
-// acc += A * B, A swizzled 64x64 (M x K), B swizzled 64x64 row-major (K x N).
+// acc += A * B, A swizzled (M x K), B swizzled row-major (K x N): b = B[k0+t][n0+g]
+// at row k0+t, physical column (n0+g) ^ (t << 2) (a per-lane constant per nb).
 __device__ __forceinline__ void mma_ab(Acc& acc, const double* sA, const double* sB, int wr, int wc, int lane) {
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll 4
-  for (int kk = 0; kk < TS; kk += 4) {
-    double a[4], b[2];
+  const int g = lane >> 2, t = lane & 3, gq = g & 3;
+  const double* pa = sA + (wr * 32 + g) * TS + t;
+  int ob[4];
 #pragma unroll
-    for (int mb = 0; mb < 4; ++mb) a[mb] = sA[swz(wr * 32 + mb * 8 + g, kk + t)];
+  for (int b = 0; b < 4; ++b) ob[b] = 4 * (b ^ gq);
+  const double* pb0 = sB + t * TS + ((wc * 16 + 0 + g) ^ (t << 2));
+  const double* pb1 = sB + t * TS + ((wc * 16 + 8 + g) ^ (t << 2));
 #pragma unroll
-    for (int nb = 0; nb < 2; ++nb) b[nb] = sB[swz(kk + t, wc * 16 + nb * 8 + g)];
+  for (int a16 = 0; a16 < TS; a16 += 16) {
 #pragma unroll
-    for (int mb = 0; mb < 4; ++mb)
+    for (int b = 0; b < 4; ++b) {
+      const int k0 = a16 + 4 * b;
+      double av[4], bv[2];
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], a[mb], b[nb]);
+      for (int mb = 0; mb < 4; ++mb) av[mb] = pa[ob[b] + mb * 8 * TS + a16];
+      bv[0] = pb0[k0 * TS];
+      bv[1] = pb1[k0 * TS];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], av[mb], bv[nb]);
+    }
   }
 }
 
-// fragment (row r0+g, cols c0+2t, c0+2t+1) <-> swizzled tile
+// fragment (row r0+g, cols c0+2t, c0+2t+1) <-> swizzled tiles (smem or global)
 template <typename F>
 __device__ __forceinline__ void acc_foreach(int wr, int wc, int lane, F f) {
   const int g = lane >> 2, t = lane & 3;
@@ -197,132 +227,139 @@ __device__ __forceinline__ void add_c22(const DenseDev& d, int tile, double* S) 
 }
 
 // ------------------------------------------------ diagonal tile factorization
-// Register-resident right-looking Cholesky of the augmented 128 x 64 panel
-// [A; I]: thread (row r in [0,128), half h) holds columns 32h..32h+31 of row r.
-// One consumer barrier per column; column k+1 is computed one step ahead and
-// the pivot of column k+2 is published early (look-ahead), so the rsqrt latency
-// overlaps the trailing update. Rows 0..63 end as L_jj (lower), rows 64..127
-// as L_jj^-T (upper).
-template <int H>
-__device__ __forceinline__ void potrf_steps(double (&a)[32], int r, CholSmem& sm, int j, int* info) {
-  constexpr int C0 = 32 * H;
+// Blocked factorization of the augmented 128 x 64 panel [A; I] held in shared
+// memory (row stride LSP, conflict-free DMMA fragments): for each 16-column
+// block, warp 0 factors the 16 x 16 diagonal block with shuffles (its lanes
+// 16..31 carry the identity rows, producing D^-T alongside), then all warps
+// solve the panel (rows below, incl. the identity rows) against D^-T and apply
+// the rank-16 trailing update on the FP64 tensor pipe. Rows 0..63 end as
+// L_jj (lower), rows 64..127 as L_jj^-T (upper). 3 consumer barriers per
+// block instead of one per column.
+constexpr int LSP = 68;        // row stride of the augmented panel (bank slots (4g + t) mod 16)
+constexpr int LDT = 20;        // row stride of the 16 x 16 D^-T block
+
+// 1/sqrt(x) for the (positive, normal) pivots without the library's
+// special-case call path, whose ABI spills the live panel registers on every
+// column: hardware approximation + two Newton steps (~1 ulp).
+__device__ __forceinline__ double pivot_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+__device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j, int* info, int lane) {
+  // lanes 0..15: row r = lane of D; lanes 16..31: identity row i = lane - 16
+  double v[16];
+  const bool drow = lane < 16;
 #pragma unroll
-  for (int k = 0; k < 63; ++k) {
-    const int k1 = k + 1, k2 = k + 2;
-    if (k == 31) {
-      // cross-half pivot of column 32: its row-32 owner (half 1) needs L[32][31]
-      if (H == 1 && r == 32) {
-        double l = sm.col[1][32];
-        double d = a[0] - l * l;
-        if (!(d > 0.0)) atomicCAS(info, 0, j * TS + 32 + 1);
-        a[0] = d;
-        sm.ipiv[0] = rsqrt(d);
-      }
-      cons_sync();
-    }
-    if (r > k) {
-      const double* colk = sm.col[k & 1];
-      const double lr = colk[r];
-      // 1) column k+1 first (look-ahead), then L[:, k+1] in its owner half
-      if (k1 >= C0 && k1 < C0 + 32) {
-        const int q1 = (k + 1) & 31;
-        const bool pub_done = (r == k1);  // its pivot publish already applied columns k-1, k (or k at 31)
-        if (!pub_done) a[q1] -= lr * colk[k1];
-        const double ip = sm.ipiv[k1 & 1];
-        if (r == k1) {
-          a[q1] = a[q1] * ip;  // L_kk = d * rsqrt(d)
-        } else {
-          const double l1 = a[q1] * ip;
-          a[q1] = l1;
-          sm.col[k1 & 1][r] = l1;
-          // 2) publish the pivot of column k+2 (same half as column k+1)
-          if (r == k2 && k2 < 64 && (k2 >> 5) == H && (k1 >> 5) == H) {
-            const int q2 = (k + 2) & 31;
-            double d = a[q2] - lr * colk[k2];
-            d = d - l1 * l1;
-            if (!(d > 0.0)) atomicCAS(info, 0, j * TS + k2 + 1);
-            a[q2] = d;
-            sm.ipiv[k2 & 1] = rsqrt(d);
-          }
-        }
-      }
-      // 3) the rest of column k's update
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const int c = C0 + q;
-        if (c <= k1) continue;
-        const bool published = (c == k2) && (r == k2) && ((k2 >> 5) == H) && ((k1 >> 5) == H);
-        if (!published) a[q] -= lr * colk[c];
+  for (int c = 0; c < 16; ++c) v[c] = drow ? S[(o + lane) * LSP + o + c] : ((c == lane - 16) ? 1.0 : 0.0);
+  int badk = -1;  // first non-positive pivot of the block
+#pragma unroll 16
+  for (int k = 0; k < 16; ++k) {
+    const double dkk = __shfl_sync(0xffffffffu, v[k], k);
+    badk = (badk < 0 && !(dkk > 0.0)) ? k : badk;
+    const double ip = pivot_rsqrt(dkk);
+    const bool active = lane > k;  // rows below the pivot (all identity lanes)
+    const double l = v[k] * ip;
+    v[k] = (lane == k) ? dkk * ip : (active ? l : v[k]);
+#pragma unroll 16
+    for (int c = 0; c < 16; ++c) {
+      if (c > k) {
+        const double lc = __shfl_sync(0xffffffffu, l, c);
+        v[c] = active ? fma(-l, lc, v[c]) : v[c];
       }
     }
-    cons_sync();
+  }
+  if (badk >= 0 && lane == 0) atomicCAS(info, 0, j * TS + o + badk + 1);
+  if (drow) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) S[(o + lane) * LSP + o + c] = (c <= lane) ? v[c] : 0.0;
+  } else {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) DT[(lane - 16) * LDT + c] = v[c];
   }
 }
 
-__device__ void potrf_aug_tile(const Acc& acc, CholSmem& sm, double* scratch, double* gL, double* gLinvT, int j,
-                               int* info, int wr, int wc, int lane) {
-  const int tid = threadIdx.x;
-  cons_sync();  // every warp has finished reading the scratch stage
-  acc_to_plain(acc, scratch, wr, wc, lane);
-  cons_sync();
-  const int h = tid >> 7, r = tid & 127;
-  double a[32];
-  if (r < 64) {
-#pragma unroll
-    for (int q = 0; q < 32; q += 2) {
-      double2 v = *reinterpret_cast<const double2*>(scratch + r * LDP + 32 * h + q);
-      a[q] = v.x;
-      a[q + 1] = v.y;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 32; ++q) a[q] = (32 * h + q == r - 64) ? 1.0 : 0.0;
-  }
-  cons_sync();  // scratch reads done before the prologue writes col[]
-  // prologue: pivot 0, column 0, pivot 1
-  if (h == 0 && r == 0) {
-    double d = a[0];
-    if (!(d > 0.0)) atomicCAS(info, 0, j * TS + 1);
-    sm.ipiv[0] = rsqrt(d);
+__device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
+                                   int* info, int wr, int wc, int lane) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  cons_sync();  // every warp has finished reading the stage area
+  acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
+    S[r * LSP + c] = acc.c[mb][nb][0];
+    S[r * LSP + c + 1] = acc.c[mb][nb][1];
+  });
+  for (int q = tid; q < 64 * 64; q += NCONS) {
+    const int r = q >> 6, c = q & 63;
+    S[(64 + r) * LSP + c] = (r == c) ? 1.0 : 0.0;
   }
   cons_sync();
-  if (h == 0) {
-    const double ip = sm.ipiv[0];
-    if (r == 0) {
-      a[0] = a[0] * ip;
-    } else {
-      const double l = a[0] * ip;
-      a[0] = l;
-      sm.col[0][r] = l;
-      if (r == 1) {
-        double d = a[1] - l * l;
-        if (!(d > 0.0)) atomicCAS(info, 0, j * TS + 2);
-        a[1] = d;
-        sm.ipiv[1] = rsqrt(d);
+#pragma unroll 1
+  for (int kb = 0; kb < 4; ++kb) {
+    const int o = 16 * kb;
+    if (warp == 0) potrf_diag16(S, DT, o, j, info, lane);
+    cons_sync();
+    // panel: rows [o+16, 128) x cols [o, o+16): P = S_panel * D^-T (in place)
+    const int rb0 = (o + 16) >> 3, nrb = 16 - rb0;
+    for (int rb = rb0 + warp; rb < 16; rb += NCONS / 32) {
+      double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+      const double* pa = S + (rb * 8 + g) * LSP + o + t;
+#pragma unroll
+      for (int k0 = 0; k0 < 16; k0 += 4) {
+        const double a = pa[k0];
+        dmma(c0[0], c0[1], a, DT[(k0 + t) * LDT + 0 + g]);
+        dmma(c1[0], c1[1], a, DT[(k0 + t) * LDT + 8 + g]);
       }
+      __syncwarp();
+      double* pw = S + (rb * 8 + g) * LSP + o + 2 * t;
+      pw[0] = c0[0];
+      pw[1] = c0[1];
+      pw[8] = c1[0];
+      pw[9] = c1[1];
+    }
+    (void)nrb;
+    cons_sync();
+    // trailing update: S[r][c] -= P[r][:] P[c][:] for c in [o+16, 64), r in [o+16, 128)
+    if (kb < 3) {
+      const int cb0 = (o + 16) >> 3, ncb = 8 - cb0;
+      const int nblk = nrb * ncb;
+      for (int bidx = warp; bidx < nblk; bidx += NCONS / 32) {
+        const int rb = rb0 + bidx / ncb, cb = cb0 + bidx % ncb;
+        if (rb < 8 && rb < cb) continue;  // strictly upper block of the L part: unused
+        double* pc = S + (rb * 8 + g) * LSP + cb * 8 + 2 * t;
+        double c0 = pc[0], c1 = pc[1];
+        const double* pa = S + (rb * 8 + g) * LSP + o + t;
+        const double* pb = S + (cb * 8 + g) * LSP + o + t;
+#pragma unroll
+        for (int k0 = 0; k0 < 16; k0 += 4) dmma(c0, c1, -pa[k0], pb[k0]);
+        pc[0] = c0;
+        pc[1] = c1;
+      }
+      cons_sync();
     }
   }
-  cons_sync();
-  if (h == 0) potrf_steps<0>(a, r, sm, j, info);
-  else potrf_steps<1>(a, r, sm, j, info);
-  // write L_jj (zero strict upper) and L_jj^-T
-  if (r < 64) {
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const int c = 32 * h + q;
-      gL[swz(r, c)] = (c <= r) ? a[q] : 0.0;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < 32; ++q) gLinvT[swz(r - 64, 32 * h + q)] = a[q];
+  // L_jj (strict upper zeroed) and L_jj^-T to global (swizzled tiles)
+  for (int q = tid; q < 64 * 64; q += NCONS) {
+    const int r = q >> 6, c = q & 63;
+    gL[swz(r, c)] = (c <= r) ? S[r * LSP + c] : 0.0;
+    gLinvT[swz(r, c)] = S[(64 + r) * LSP + c];
   }
 }
 
 // ---------------------------------------------------------------- kernel
 __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, const int2* __restrict__ tasks,
                                                                 int ntasks) {
-  extern __shared__ __align__(1024) unsigned char smraw[];
-  CholSmem& sm = *reinterpret_cast<CholSmem*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+  extern __shared__ __align__(128) double smd[];
+  CholSmem sm;
+  sm.stage0 = smd;
+  sm.col = smd + SM_COL;
+  sm.ipiv = smd + SM_IPIV;
+  sm.full = reinterpret_cast<unsigned long long*>(smd + SM_BAR);
+  sm.empty = sm.full + NSTAGE;
+  sm.task = reinterpret_cast<int*>(sm.empty + NSTAGE);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool producer = warp == 8;
   const int wr = warp >> 2, wc = warp & 3;
@@ -330,44 +367,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
   const int ntiles = N * (N + 1) / 2;
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&sm.full[s], SPB_CHOL_CPASYNC ? 32 : 1);
+      mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], NCONS / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   int it = 0;  // stage-use counter, advanced identically by producer and consumers
+  unsigned long long t_claim = 0, t_kdone = 0, t_fin = 0;
   for (;;) {
-    if (tid == 0) sm.task = atomicAdd(d.counter, 1);
+    if (tid == 0) *sm.task = atomicAdd(d.counter, 1);
     __syncthreads();
-    const int task = sm.task;
+    const int task = *sm.task;
     if (task >= ntasks) break;
     const int2 ij = tasks[task];
     const int i = ij.x, j = ij.y;
     const bool rhs = (i == N);
+    if (d.trace && tid == 0) t_claim = globaltimer();
     int* myflag = d.flags + (rhs ? ntiles + j : tidx(i, j));
 
     if (producer) {
-      // the whole producer warp walks the task; lane 0 polls flags / waits for
-      // free stages, then the tiles are streamed into the stage ring
+      // lane 0 polls flags, waits for a free stage and issues one 32 KB bulk
+      // copy (TMA) per tile into the stage ring
       auto fill = [&](const double* a, const double* b, int slot_a) {
         const int s = it % NSTAGE;
-        if (lane == 0) mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
-        __syncwarp();
-#if SPB_CHOL_CPASYNC
-        // generic-proxy path: 16-byte cp.async per lane, completion tracked on
-        // full[s] by one noinc arrive per lane (count 32)
-        for (int q = lane; q < TILE / 2; q += 32) cp_async16(sm.stage[s][slot_a] + 2 * q, a + 2 * q);
-        if (b)
-          for (int q = lane; q < TILE / 2; q += 32) cp_async16(sm.stage[s][1] + 2 * q, b + 2 * q);
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&sm.full[s])) : "memory");
-#else
         if (lane == 0) {
+          mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
           mbar_expect_tx(&sm.full[s], (b ? 2 : 1) * TILE_BYTES);
-          bulk_g2s(sm.stage[s][slot_a], a, TILE_BYTES, &sm.full[s]);
-          if (b) bulk_g2s(sm.stage[s][1], b, TILE_BYTES, &sm.full[s]);
         }
-#endif
+        if (lane == 0) {
+          bulk_g2s(sm.slot(s, slot_a), a, TILE_BYTES, &sm.full[s]);
+          if (b) bulk_g2s(sm.slot(s, 1), b, TILE_BYTES, &sm.full[s]);
+        }
+        __syncwarp();
         ++it;
       };
       auto wait_ready = [&](const int* f) {
@@ -391,10 +423,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       int s = it % NSTAGE;
       mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
       if (!rhs && d.c22_tile_ptr) {
-        add_c22(d, tidx(i, j), sm.stage[s][0]);
+        add_c22(d, tidx(i, j), sm.slot(s, 0));
         cons_sync();
       }
-      smem_to_acc(acc, sm.stage[s][0], wr, wc, lane);
+      smem_to_acc(acc, sm.slot(s, 0), wr, wc, lane);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -404,19 +436,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       for (int k = 0; k < j; ++k) {
         s = it % NSTAGE;
         mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-        mma_abt<true>(acc, sm.stage[s][0], sm.stage[s][1], wr, wc, lane);
+        mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         last = s;
         ++it;
       }
       // ---- finalize
+      if (d.trace && tid == 0) t_kdone = globaltimer();
       if (i == j) {
         // stages are idle until the next task: use the last one as scratch
-        potrf_aug_tile(acc, sm, sm.stage[last][0], d.L + (size_t)tidx(j, j) * TILE, d.LinvT + (size_t)j * TILE, j,
-                       d.info, wr, wc, lane);
+        // the whole stage area is idle until the next task: augmented panel + D^-T
+        potrf_blocked_tile(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
+                           d.LinvT + (size_t)j * TILE, j, d.info, wr, wc, lane);
       } else {
-        double* scratch = sm.stage[last][0];
+        double* scratch = sm.slot(last, 0);
         cons_sync();  // every warp has finished reading stage `last`
         acc_to_swz(acc, scratch, wr, wc, lane);
         cons_sync();
@@ -424,19 +458,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
         mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
         Acc out;
         acc_zero(out);
-        mma_ab(out, scratch, sm.stage[s][1], wr, wc, lane);  // acc * inv(L_jj)^T = acc * LinvT
+        mma_ab(out, scratch, sm.slot(s, 1), wr, wc, lane);  // acc * inv(L_jj)^T = acc * LinvT
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         ++it;
         double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
         acc_to_swz(out, dst, wr, wc, lane);
       }
+      if (d.trace && tid == 0) t_fin = globaltimer();
       fence_proxy_async_smem();    // generic smem writes before later bulk copies into the stages
       fence_proxy_async_global();  // generic global tile stores before other CTAs' bulk reads
       __threadfence();
     }
     __syncthreads();
-    if (tid == 0) st_release(myflag, 1);
+    if (tid == 0) {
+      st_release(myflag, 1);
+      if (d.trace) {
+        unsigned long long* tr = d.trace + 4 * (size_t)task;
+        tr[0] = t_claim;
+        tr[1] = t_kdone;
+        tr[2] = globaltimer();
+        tr[3] = t_fin;
+      }
+    }
   }
 }
 

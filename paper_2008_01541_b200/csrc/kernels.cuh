@@ -61,6 +61,7 @@ struct DenseDev {
   const double* proxy_w;
   const double* proxy_c;
   const uint8_t* active;
+  unsigned long long* trace;  // optional: per task {claim, k-loop done, finalize done, sm}
 };
 int dense_tile_count(int N);
 size_t cholesky_smem_bytes();

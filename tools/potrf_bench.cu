@@ -1,0 +1,75 @@
+// Microbenchmark of the diagonal-tile factorization pieces (diagnostics).
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2008_01541_b200/csrc potrf_bench.cu ...
+#include "../paper_2008_01541_b200/csrc/dense.cu"
+
+namespace spb {
+void set_error(const std::string&) {}
+}
+using namespace spb;
+
+__global__ void __launch_bounds__(288, 1) k_potrf_bench(const double* A, double* L, double* LiT, int* info,
+                                                       long long* cycles, int reps) {
+  extern __shared__ __align__(128) double smd[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 8) return;  // consumers only (named barrier 1 counts 256)
+  const int wr = warp >> 2, wc = warp & 3;
+  Acc acc;
+  acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
+    acc.c[mb][nb][0] = A[r * 64 + c];
+    acc.c[mb][nb][1] = A[r * 64 + c + 1];
+  });
+  long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) potrf_blocked_tile(acc, smd, smd + 128 * LSP, L, LiT, 0, info, wr, wc, lane);
+  long long t1 = clock64();
+  // diag16 alone
+  for (int r = 0; r < reps; ++r) {
+    if (warp == 0) potrf_diag16(smd, smd + 128 * LSP, 0, 0, info, lane);
+    cons_sync();
+  }
+  long long t2 = clock64();
+  for (int r = 0; r < reps; ++r) cons_sync();
+  long long t3 = clock64();
+  if (tid == 0) {
+    cycles[0] = (t1 - t0) / reps;
+    cycles[1] = (t2 - t1) / reps;
+    cycles[2] = (t3 - t2) / reps;
+  }
+}
+
+int main() {
+  double hA[4096];
+  for (int r = 0; r < 64; ++r)
+    for (int c = 0; c < 64; ++c) hA[r * 64 + c] = (r == c ? 100.0 : 0.0) + 1.0 / (1.0 + r + c);
+  double *A, *L, *LiT;
+  int* info;
+  long long* cyc;
+  cudaMalloc(&A, 4096 * 8);
+  cudaMalloc(&L, 4096 * 8);
+  cudaMalloc(&LiT, 4096 * 8);
+  cudaMalloc(&info, 4);
+  cudaMalloc(&cyc, 3 * 8);
+  cudaMemset(info, 0, 4);
+  cudaMemcpy(A, hA, 4096 * 8, cudaMemcpyHostToDevice);
+  size_t smem = cholesky_smem_bytes();
+  cudaFuncSetAttribute(k_potrf_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_potrf_bench<<<1, 288, smem>>>(A, L, LiT, info, cyc, 20);
+  cudaDeviceSynchronize();
+  long long h[3];
+  cudaMemcpy(h, cyc, 24, cudaMemcpyDeviceToHost);
+  int hi;
+  cudaMemcpy(&hi, info, 4, cudaMemcpyDeviceToHost);
+  printf("err=%s info=%d potrf_blocked %lld cyc (%.2f us @1.9GHz), diag16 %lld cyc, cons_sync %lld cyc\n",
+         cudaGetErrorString(cudaGetLastError()), hi, h[0], h[0] / 1900.0, h[1], h[2]);
+  double hL[4096];
+  cudaMemcpy(hL, L, 4096 * 8, cudaMemcpyDeviceToHost);
+  // check L L^T == A
+  double err = 0;
+  for (int r = 0; r < 64; ++r)
+    for (int c = 0; c <= r; ++c) {
+      double s = 0;
+      for (int k = 0; k <= c; ++k) s += hL[swz(r, k)] * hL[swz(c, k)];
+      err = fmax(err, fabs(s - hA[r * 64 + c]));
+    }
+  printf("max |LL^T - A| = %.3e\n", err);
+  return 0;
+}
