@@ -46,7 +46,8 @@ def _env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms (continuous
+    `-lms` query) while the timed region runs."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -54,41 +55,70 @@ class ClockSampler:
 
     def __init__(self, gpu: int):
         self.gpu = gpu
+        self.proc = None
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) == 7:
-                    self.samples.append(vals)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the first sample land before the timed work starts
+        except Exception:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=6)
+        if self.proc is None:
+            return
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.splitlines():
+            vals = [v.strip() for v in line.split(",")]
+            if len(vals) == 7:
+                self.samples.append(vals)
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        sm = [x for x in (num(s[0]) for s in self.samples) if x is not None]
+        mx = [x for x in (num(s[1]) for s in self.samples) if x is not None]
+        pw = [x for x in (num(s[2]) for s in self.samples) if x is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "power_w_max": max(pw) if pw else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+def max_over_ranks(dist, v: float) -> float:
+    """The slowest rank's time (replicas: one scene per GPU). NCCL reduces on
+    the device, gloo (CPU tests) on the host."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return v
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(world: int, ms_per_frame_max: float) -> float:
+    """Whole-job frames/s: every rank solves its own scene, so N frames land
+    per slowest-rank frame time."""
+    return world * 1e3 / ms_per_frame_max
 
 
 def build_sim(config: str, outer: int, inner: int):
@@ -151,7 +181,10 @@ def run_reference(args):
     sim, setup_s = build_sim(args.config, args.outer, args.inner)
     for _ in range(args.warmup):
         pass
-    sec, times = cpu_oracle_frames(sim, max(1, args.steps), threads)
+    # bounded sample: at most --ref-frames frames of the workload (the oracle
+    # takes ~1.5 s per 600K frame on 16 cores), reported as frames/s
+    nf = max(1, min(args.steps, args.ref_frames))
+    sec, times = cpu_oracle_frames(sim, nf, threads)
     value = 1.0 / sec
     line = {
         "impl": "reference", "metric": "PD frames/sec w/ collisions (600K tets, 5% collision DOFs)",
@@ -208,20 +241,15 @@ def run_b200(args):
             dist.barrier()
 
     def allmax(v):
-        if dist is None:
-            return v
-        import torch
-
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return max_over_ranks(dist, v)
 
     # ---- device-resident frames (value)
     ms = ctypes.c_double(0)
     phase = (ctypes.c_double * 5)()
+    clk = ClockSampler(local)
+    clk.__enter__()
     barrier()
-    with ClockSampler(local) as clk:
-        _native.check(lib.spb_ctx_bench(ds.handle, ctypes.byref(cfg), args.steps, ctypes.byref(ms), phase))
+    _native.check(lib.spb_ctx_bench(ds.handle, ctypes.byref(cfg), args.steps, ctypes.byref(ms), phase))
     ms_frame = allmax(ms.value)
     # ---- dense Cholesky alone
     chol = ctypes.c_double(0)
@@ -234,6 +262,7 @@ def run_b200(args):
     for _ in range(args.steps):
         met = sim.step()
     e2e_s = allmax((time.perf_counter() - t0) / args.steps)
+    clk.__exit__(None, None, None)
     launches = int(met_launches(ds, cfg)) * args.steps
     n, P_, na = sim.mesh.num_nodes, len(sim.model.proxies), len(sim.model.attachments)
     h2d = 24 * n + P_ + 24 * P_ + 24 * na + 32 * 104
@@ -246,7 +275,7 @@ def run_b200(args):
     achieved = chol_flops / (chol.value * 1e-3) / 1e12
     line = {
         "metric": "PD frames/sec w/ collisions (600K tets, 5% collision DOFs); Cholesky FP64 TFLOPS",
-        "value": world * 1e3 / ms_frame, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+        "value": replica_throughput(world, ms_frame), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_frame, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (lattice scene through the reference schema)",
         "config": _config_dict(sim, args),
@@ -286,13 +315,14 @@ def met_launches(ds, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg5"])
     ap.add_argument("--outer", type=int, default=1)
     ap.add_argument("--inner", type=int, default=1)
     ap.add_argument("--cpu-frames", type=int, default=3)
+    ap.add_argument("--ref-frames", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -139,6 +139,8 @@ struct Ctx {
   ColliderSet* cols_host = nullptr;  // pinned
   DBuf<ColliderSet> cols_dev;
   double* att_tgt_host = nullptr;    // pinned staging
+  char* io_host = nullptr;           // pinned staging for set_state / get_state
+  size_t io_bytes = 0;
   // metrics
   DBuf<double> e_part, a_part, p_part, r_part, metrics_out;
   double* metrics_host = nullptr;    // pinned
@@ -159,6 +161,7 @@ struct Ctx {
     for (double* v : shape_vals) cudaFree(v);
     if (cols_host) cudaFreeHost(cols_host);
     if (att_tgt_host) cudaFreeHost(att_tgt_host);
+    if (io_host) cudaFreeHost(io_host);
     if (metrics_host) cudaFreeHost(metrics_host);
     if (st) cudaStreamDestroy(st);
   }
@@ -166,7 +169,58 @@ struct Ctx {
   int create(const spb_scene_desc* s, Factor* f, int dev);
   int enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev /* 7 phase events or null */);
   int sync_shapes();
+  int io_reserve(size_t bytes) {
+    if (bytes <= io_bytes) return SPB_OK;
+    if (io_host) cudaFreeHost(io_host);
+    io_host = nullptr;
+    io_bytes = 0;
+    SPB_CUDA(cudaMallocHost(&io_host, bytes));
+    io_bytes = bytes;
+    return SPB_OK;
+  }
 };
+
+// Host <-> device state copies go through one pinned staging area: a plain
+// memcpy into pinned memory plus async DMA on the context stream, instead of
+// the driver's chunked pageable path.
+struct IoList {
+  struct Item { void* dev; void* host; size_t bytes; };
+  Item items[8];
+  int n = 0;
+  size_t total = 0;
+  void add(void* dev, const void* host, size_t bytes) {
+    if (!host || !bytes) return;
+    items[n++] = Item{dev, const_cast<void*>(host), bytes};
+    total += (bytes + 255) & ~size_t(255);
+  }
+};
+
+static int io_upload(Ctx* c, const IoList& l) {
+  TRY(c->io_reserve(l.total));
+  size_t off = 0;
+  for (int i = 0; i < l.n; ++i) {
+    memcpy(c->io_host + off, l.items[i].host, l.items[i].bytes);
+    SPB_CUDA(cudaMemcpyAsync(l.items[i].dev, c->io_host + off, l.items[i].bytes, cudaMemcpyHostToDevice, c->st));
+    off += (l.items[i].bytes + 255) & ~size_t(255);
+  }
+  return SPB_OK;
+}
+
+static int io_download(Ctx* c, const IoList& l) {
+  TRY(c->io_reserve(l.total));
+  size_t off = 0;
+  for (int i = 0; i < l.n; ++i) {
+    SPB_CUDA(cudaMemcpyAsync(c->io_host + off, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, c->st));
+    off += (l.items[i].bytes + 255) & ~size_t(255);
+  }
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  off = 0;
+  for (int i = 0; i < l.n; ++i) {
+    memcpy(l.items[i].host, c->io_host + off, l.items[i].bytes);
+    off += (l.items[i].bytes + 255) & ~size_t(255);
+  }
+  return SPB_OK;
+}
 
 int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   device = dev;
@@ -453,6 +507,9 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
 
 using spb::Ctx;
 using spb::Factor;
+using spb::IoList;
+using spb::io_upload;
+using spb::io_download;
 
 // ================================================================== C ABI
 extern "C" {
@@ -541,7 +598,13 @@ int32_t spb_ctx_set_state(spb_ctx* cp, const double* x, const double* R, const d
   Ctx* c = reinterpret_cast<Ctx*>(cp);
   SPB_CUDA(cudaSetDevice(c->device));
   SPB_CUDA(cudaStreamSynchronize(c->st));
-  if (x) SPB_CUDA(cudaMemcpy(c->x.p, x, sizeof(double) * 3 * c->n, cudaMemcpyHostToDevice));
+  IoList l;
+  l.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  if (c->P) l.add(c->active.p, active, c->P);
+  if (c->P) l.add(c->target.p, target, sizeof(double) * 3 * c->P);
+  if (c->n2) l.add(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2);
+  if (c->n2) l.add(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2);
+  TRY(io_upload(c, l));
   std::vector<double> soa;
   if (R) {
     spb::to_soa9(R, c->ne, soa);
@@ -551,12 +614,6 @@ int32_t spb_ctx_set_state(spb_ctx* cp, const double* x, const double* R, const d
     spb::to_soa9(Q, c->ne, soa);
     SPB_CUDA(cudaMemcpy(c->Q.p, soa.data(), sizeof(double) * 9 * c->ne, cudaMemcpyHostToDevice));
   }
-  if (active && c->P) SPB_CUDA(cudaMemcpy(c->active.p, active, c->P, cudaMemcpyHostToDevice));
-  if (target && c->P) SPB_CUDA(cudaMemcpy(c->target.p, target, sizeof(double) * 3 * c->P, cudaMemcpyHostToDevice));
-  if (f_tilde2 && c->n2)
-    SPB_CUDA(cudaMemcpy(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2, cudaMemcpyHostToDevice));
-  if (u2_accum && c->n2)
-    SPB_CUDA(cudaMemcpy(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2, cudaMemcpyHostToDevice));
   return SPB_OK;
   SPB_GUARD_END
 }
@@ -567,7 +624,13 @@ int32_t spb_ctx_get_state(spb_ctx* cp, double* x, double* R, double* Q, uint8_t*
   Ctx* c = reinterpret_cast<Ctx*>(cp);
   SPB_CUDA(cudaSetDevice(c->device));
   SPB_CUDA(cudaStreamSynchronize(c->st));
-  if (x) SPB_CUDA(cudaMemcpy(x, c->x.p, sizeof(double) * 3 * c->n, cudaMemcpyDeviceToHost));
+  IoList l;
+  l.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  if (c->P) l.add(c->active.p, active, c->P);
+  if (c->P) l.add(c->target.p, target, sizeof(double) * 3 * c->P);
+  if (c->n2) l.add(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2);
+  if (c->n2) l.add(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2);
+  TRY(io_download(c, l));
   auto soa_down = [&](const double* d, double* h) -> int {
     std::vector<double> soa(9 * c->ne);
     SPB_CUDA(cudaMemcpy(soa.data(), d, sizeof(double) * 9 * c->ne, cudaMemcpyDeviceToHost));
@@ -577,12 +640,6 @@ int32_t spb_ctx_get_state(spb_ctx* cp, double* x, double* R, double* Q, uint8_t*
   };
   if (R) TRY(soa_down(c->R.p, R));
   if (Q && c->ep.biphasic) TRY(soa_down(c->Q.p, Q));
-  if (active && c->P) SPB_CUDA(cudaMemcpy(active, c->active.p, c->P, cudaMemcpyDeviceToHost));
-  if (target && c->P) SPB_CUDA(cudaMemcpy(target, c->target.p, sizeof(double) * 3 * c->P, cudaMemcpyDeviceToHost));
-  if (f_tilde2 && c->n2)
-    SPB_CUDA(cudaMemcpy(f_tilde2, c->f_tilde2.p, sizeof(double) * 3 * c->n2, cudaMemcpyDeviceToHost));
-  if (u2_accum && c->n2)
-    SPB_CUDA(cudaMemcpy(u2_accum, c->u2acc.p, sizeof(double) * 3 * c->n2, cudaMemcpyDeviceToHost));
   return SPB_OK;
   SPB_GUARD_END
 }
