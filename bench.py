@@ -121,6 +121,16 @@ def replica_throughput(world: int, ms_per_frame_max: float) -> float:
     return world * 1e3 / ms_per_frame_max
 
 
+def committed_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_cholesky_tiles
+    launch from the newest committed `ncu --set full` capture (profiles/)."""
+    caps = sorted((ROOT / "profiles").glob("r*_cholesky_traffic.json"))
+    if not caps:
+        return None, None
+    js = json.loads(caps[-1].read_text())
+    return js.get("traffic_bytes"), f"profiles/{caps[-1].name} (ncu --set full, one launch)"
+
+
 def build_sim(config: str, outer: int, inner: int):
     import paper_2008_01541_b200 as P
     from scenes import config_yaml
@@ -272,6 +282,7 @@ def run_b200(args):
             dist.destroy_process_group()
         return
     fp64_peak = measure_fp64_peak()
+    traffic, traffic_src = committed_traffic()
     achieved = chol_flops / (chol.value * 1e-3) / 1e12
     line = {
         "metric": "PD frames/sec w/ collisions (600K tets, 5% collision DOFs); Cholesky FP64 TFLOPS",
@@ -284,7 +295,8 @@ def run_b200(args):
         "phases_ms": {"local_alpha+forces": phase[0], "forward_sweep": phase[1], "inner_loop": phase[2],
                       "backward_sweep": phase[3], "metrics": phase[4]},
         "roofline": {"bound": "tensor", "kernel": "k_cholesky_tiles (FP64 DMMA)", "achieved": achieved,
-                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+                     "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                      "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (MEASURED_PEAKS.json has no FP64)",
                      "flops_per_launch": chol_flops},
         "gpu_launches": launches, "setup_s": setup_s,

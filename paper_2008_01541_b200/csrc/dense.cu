@@ -148,6 +148,40 @@ __device__ __forceinline__ void mma_abt(Acc& acc, const double* sA, const double
   }
 }
 
+// Fused diagonal task: accD -= A A^T and accO -= A B^T in one pass, sharing
+// the A fragments (A = L_Jk, B = L_{J-1,k}).
+__device__ __forceinline__ void mma_abt_dual(Acc& accD, Acc& accO, const double* sA, const double* sB, int wr,
+                                             int wc, int lane) {
+  const int g = lane >> 2, t = lane & 3, gq = g & 3;
+  const double* pa = sA + (wr * 32 + g) * TS + t;
+  const double* pd = sA + (wc * 16 + g) * TS + t;
+  const double* po = sB + (wc * 16 + g) * TS + t;
+  int ob[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) ob[b] = 4 * (b ^ gq);
+#pragma unroll
+  for (int a16 = 0; a16 < TS; a16 += 16) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double av[4], bd[2], bo[2];
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) av[mb] = -pa[ob[b] + mb * 8 * TS + a16];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        bd[nb] = pd[ob[b] + nb * 8 * TS + a16];
+        bo[nb] = po[ob[b] + nb * 8 * TS + a16];
+      }
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb)
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) {
+          dmma(accD.c[mb][nb][0], accD.c[mb][nb][1], av[mb], bd[nb]);
+          dmma(accO.c[mb][nb][0], accO.c[mb][nb][1], av[mb], bo[nb]);
+        }
+    }
+  }
+}
+
 // acc += A * B, A swizzled (M x K), B swizzled row-major (K x N): b = B[k0+t][n0+g]
 // at row k0+t, physical column (n0+g) ^ (t << 2) (a per-lane constant per nb).
 __device__ __forceinline__ void mma_ab(Acc& acc, const double* sA, const double* sB, int wr, int wc, int lane) {
@@ -408,7 +442,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       };
       const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
       fill(src, nullptr, 0);
-      for (int k = 0; k < j; ++k) {
+      if (i == j && j > 0) {
+        // fused diagonal task: also produce the sub-diagonal tile (j, j-1)
+        fill(d.sigma0 + (size_t)tidx(j, j - 1) * TILE, nullptr, 0);
+        for (int k = 0; k < j - 1; ++k) {
+          wait_ready(d.flags + tidx(j, k));
+          wait_ready(d.flags + tidx(j - 1, k));
+          fill(d.L + (size_t)tidx(j, k) * TILE, d.L + (size_t)tidx(j - 1, k) * TILE, 0);
+        }
+        wait_ready(d.flags + tidx(j - 1, j - 1));
+        fill(d.LinvT + (size_t)(j - 1) * TILE, nullptr, 1);
+      } else for (int k = 0; k < j; ++k) {
         wait_ready(d.flags + (rhs ? ntiles + k : tidx(i, k)));
         wait_ready(d.flags + tidx(j, k));
         fill(rhs ? d.Y + (size_t)k * TILE : d.L + (size_t)tidx(i, k) * TILE, d.L + (size_t)tidx(j, k) * TILE, 0);
@@ -432,8 +476,53 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       int last = s;
       ++it;
-      // ---- left-looking accumulation over k < j
-      for (int k = 0; k < j; ++k) {
+      if (i == j && j > 0) {
+        // ---- fused diagonal task: accO <- H(j, j-1), dual accumulation over
+        // k < j-1, then L(j, j-1) = accO inv(L_{j-1,j-1})^T is finalized and
+        // published here and its rank-64 update applied locally, so the
+        // critical chain diag(j-1) -> diag(j) crosses one flag instead of two
+        Acc accO;
+        s = it % NSTAGE;
+        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+        if (d.c22_tile_ptr) {
+          add_c22(d, tidx(j, j - 1), sm.slot(s, 0));
+          cons_sync();
+        }
+        smem_to_acc(accO, sm.slot(s, 0), wr, wc, lane);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        ++it;
+        for (int k = 0; k < j - 1; ++k) {
+          s = it % NSTAGE;
+          mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+          mma_abt_dual(acc, accO, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.empty[s]);
+          ++it;
+        }
+        s = it % NSTAGE;
+        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);  // slot 1: inv(L_{j-1,j-1})^T
+        // slot 0 of this stage was last read three stage-uses ago by every
+        // warp (the producer refilled the stage after all arrived): scratch
+        double* scratch = sm.slot(s, 0);
+        acc_to_swz(accO, scratch, wr, wc, lane);
+        cons_sync();
+        Acc out;
+        acc_zero(out);
+        mma_ab(out, scratch, sm.slot(s, 1), wr, wc, lane);
+        acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+        cons_sync();  // every warp has finished reading scratch and the LinvT tile
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        ++it;
+        acc_to_swz(out, scratch, wr, wc, lane);
+        fence_proxy_async_global();
+        __threadfence();
+        cons_sync();
+        if (tid == 0) st_release(d.flags + tidx(j, j - 1), 1);
+        mma_abt<true>(acc, scratch, scratch, wr, wc, lane);
+      } else for (int k = 0; k < j; ++k) {
+        // ---- left-looking accumulation over k < j
         s = it % NSTAGE;
         mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
         mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
@@ -689,7 +778,8 @@ std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead) {
       tk.push_back(make_int2(next_diag, next_diag));
       ++next_diag;
     }
-    for (int i = j + 1; i < N; ++i) tk.push_back(make_int2(i, j));
+    // (j+1, j) is produced by the fused diagonal task j+1
+    for (int i = j + 2; i < N; ++i) tk.push_back(make_int2(i, j));
     if (with_rhs) tk.push_back(make_int2(N, j));
   }
   return tk;

@@ -35,7 +35,7 @@ rows = []
 for j in range(N):
     pot = done[(j, j)] - kd[(j, j)]
     trsm = done[(j + 1, j)] - done[(j, j)] if (j + 1, j) in done else float("nan")
-    wait = kd[(j, j)] - done[(j, j - 1)] if j > 0 else float("nan")
+    wait = kd[(j, j)] - done.get((j, j - 1), float("nan")) if j > 0 else float("nan")
     rows.append((pot, trsm, wait))
     if j % 8 == 0 or j == N - 1:
         print(f"{j:3d} {cl[(j,j)]:7.1f} {kd[(j,j)]:7.1f} {done[(j,j)]:7.1f} | {pot:6.2f} {trsm:8.2f} {wait:10.2f}")
