@@ -97,9 +97,9 @@ __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"
 
 // Spin (one thread) until a readiness flag is set, then order later reads
 // (generic and async proxy) after the producer's release.
-__device__ __forceinline__ void poll_flag(const int* f) {
-  if (ld_relaxed(f) == 0) {
-    while (ld_relaxed(f) == 0) __nanosleep(32);
+__device__ __forceinline__ void poll_flag(const int* f, int v) {
+  if (ld_relaxed(f) < v) {
+    while (ld_relaxed(f) < v) __nanosleep(32);
   }
   fence_acq_rel_gpu();
   fence_proxy_async_global();
@@ -144,40 +144,6 @@ __device__ __forceinline__ void mma_abt(Acc& acc, const double* sA, const double
       for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], av[mb], bv[nb]);
-    }
-  }
-}
-
-// Fused diagonal task: accD -= A A^T and accO -= A B^T in one pass, sharing
-// the A fragments (A = L_Jk, B = L_{J-1,k}).
-__device__ __forceinline__ void mma_abt_dual(Acc& accD, Acc& accO, const double* sA, const double* sB, int wr,
-                                             int wc, int lane) {
-  const int g = lane >> 2, t = lane & 3, gq = g & 3;
-  const double* pa = sA + (wr * 32 + g) * TS + t;
-  const double* pd = sA + (wc * 16 + g) * TS + t;
-  const double* po = sB + (wc * 16 + g) * TS + t;
-  int ob[4];
-#pragma unroll
-  for (int b = 0; b < 4; ++b) ob[b] = 4 * (b ^ gq);
-#pragma unroll
-  for (int a16 = 0; a16 < TS; a16 += 16) {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      double av[4], bd[2], bo[2];
-#pragma unroll
-      for (int mb = 0; mb < 4; ++mb) av[mb] = -pa[ob[b] + mb * 8 * TS + a16];
-#pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        bd[nb] = pd[ob[b] + nb * 8 * TS + a16];
-        bo[nb] = po[ob[b] + nb * 8 * TS + a16];
-      }
-#pragma unroll
-      for (int mb = 0; mb < 4; ++mb)
-#pragma unroll
-        for (int nb = 0; nb < 2; ++nb) {
-          dmma(accD.c[mb][nb][0], accD.c[mb][nb][1], av[mb], bd[nb]);
-          dmma(accO.c[mb][nb][0], accO.c[mb][nb][1], av[mb], bo[nb]);
-        }
     }
   }
 }
@@ -436,30 +402,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
         __syncwarp();
         ++it;
       };
-      auto wait_ready = [&](const int* f) {
-        if (lane == 0) poll_flag(f);
+      auto wait_ready = [&](const int* f, int v) {
+        if (lane == 0) poll_flag(f, v);
         __syncwarp();
       };
+      // flag values: 1 = final; the sub-diagonal tile (k+1, k) is first
+      // published as a partial sum (1) and finalized by diagonal task k+1 (2)
+      auto tile_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), r == c + 1 ? 2 : 1); };
       const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
       fill(src, nullptr, 0);
-      if (i == j && j > 0) {
-        // fused diagonal task: also produce the sub-diagonal tile (j, j-1)
-        fill(d.sigma0 + (size_t)tidx(j, j - 1) * TILE, nullptr, 0);
+      if (i == j) {
+        // diagonal task: A = B = L_jk (one copy), then the partial sum of the
+        // sub-diagonal tile (j, j-1) with inv(L_{j-1,j-1})^T for its finalize
         for (int k = 0; k < j - 1; ++k) {
-          wait_ready(d.flags + tidx(j, k));
-          wait_ready(d.flags + tidx(j - 1, k));
-          fill(d.L + (size_t)tidx(j, k) * TILE, d.L + (size_t)tidx(j - 1, k) * TILE, 0);
+          tile_ready(j, k);
+          fill(d.L + (size_t)tidx(j, k) * TILE, nullptr, 0);
         }
-        wait_ready(d.flags + tidx(j - 1, j - 1));
-        fill(d.LinvT + (size_t)(j - 1) * TILE, nullptr, 1);
-      } else for (int k = 0; k < j; ++k) {
-        wait_ready(d.flags + (rhs ? ntiles + k : tidx(i, k)));
-        wait_ready(d.flags + tidx(j, k));
-        fill(rhs ? d.Y + (size_t)k * TILE : d.L + (size_t)tidx(i, k) * TILE, d.L + (size_t)tidx(j, k) * TILE, 0);
-      }
-      if (i != j) {
-        wait_ready(d.flags + tidx(j, j));
-        fill(d.LinvT + (size_t)j * TILE, nullptr, 1);
+        if (j > 0) {
+          wait_ready(d.flags + tidx(j, j - 1), 1);
+          wait_ready(d.flags + tidx(j - 1, j - 1), 1);
+          fill(d.L + (size_t)tidx(j, j - 1) * TILE, d.LinvT + (size_t)(j - 1) * TILE, 0);
+        }
+      } else {
+        for (int k = 0; k < j; ++k) {
+          if (rhs) wait_ready(d.flags + ntiles + k, 1);
+          else tile_ready(i, k);
+          tile_ready(j, k);
+          fill(rhs ? d.Y + (size_t)k * TILE : d.L + (size_t)tidx(i, k) * TILE, d.L + (size_t)tidx(j, k) * TILE, 0);
+        }
+        if (i != j + 1 || rhs) {
+          wait_ready(d.flags + tidx(j, j), 1);
+          fill(d.LinvT + (size_t)j * TILE, nullptr, 1);
+        }
       }
     } else {
       // ---- consumers: acc <- H tile (sigma0 + C22) or the g^T tile
@@ -476,68 +450,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       int last = s;
       ++it;
-      if (i == j && j > 0) {
-        // ---- fused diagonal task: accO <- H(j, j-1), dual accumulation over
-        // k < j-1, then L(j, j-1) = accO inv(L_{j-1,j-1})^T is finalized and
-        // published here and its rank-64 update applied locally, so the
-        // critical chain diag(j-1) -> diag(j) crosses one flag instead of two
-        Acc accO;
+      const int nk = (i == j) ? j - 1 : j;  // the diagonal task's last k comes from the partial
+      for (int k = 0; k < nk; ++k) {
+        // ---- left-looking accumulation
         s = it % NSTAGE;
         mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-        if (d.c22_tile_ptr) {
-          add_c22(d, tidx(j, j - 1), sm.slot(s, 0));
-          cons_sync();
-        }
-        smem_to_acc(accO, sm.slot(s, 0), wr, wc, lane);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
-        ++it;
-        for (int k = 0; k < j - 1; ++k) {
-          s = it % NSTAGE;
-          mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-          mma_abt_dual(acc, accO, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.empty[s]);
-          ++it;
-        }
-        s = it % NSTAGE;
-        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);  // slot 1: inv(L_{j-1,j-1})^T
-        // slot 0 of this stage was last read three stage-uses ago by every
-        // warp (the producer refilled the stage after all arrived): scratch
-        double* scratch = sm.slot(s, 0);
-        acc_to_swz(accO, scratch, wr, wc, lane);
-        cons_sync();
-        Acc out;
-        acc_zero(out);
-        mma_ab(out, scratch, sm.slot(s, 1), wr, wc, lane);
-        acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
-        cons_sync();  // every warp has finished reading scratch and the LinvT tile
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
-        ++it;
-        acc_to_swz(out, scratch, wr, wc, lane);
-        fence_proxy_async_global();
-        __threadfence();
-        cons_sync();
-        if (tid == 0) st_release(d.flags + tidx(j, j - 1), 1);
-        mma_abt<true>(acc, scratch, scratch, wr, wc, lane);
-      } else for (int k = 0; k < j; ++k) {
-        // ---- left-looking accumulation over k < j
-        s = it % NSTAGE;
-        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-        mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
+        mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, i == j ? 0 : 1), wr, wc, lane);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         last = s;
         ++it;
       }
+      if (i == j && j > 0) {
+        // ---- finalize the sub-diagonal tile on the critical chain:
+        // L(j, j-1) = partial * inv(L_{j-1,j-1})^T, publish it (flag 2), and
+        // apply its rank-64 update here; diag(j-1) -> diag(j) crosses one flag
+        s = it % NSTAGE;
+        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+        Acc out;
+        acc_zero(out);
+        mma_ab(out, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
+        acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+        cons_sync();  // every warp has finished reading the stage
+        double* scratch = sm.slot(s, 0);
+        acc_to_swz(out, scratch, wr, wc, lane);
+        fence_proxy_async_global();
+        __threadfence();
+        cons_sync();
+        if (tid == 0) st_release(d.flags + tidx(j, j - 1), 2);
+        mma_abt<true>(acc, scratch, scratch, wr, wc, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        ++it;
+      }
       // ---- finalize
       if (d.trace && tid == 0) t_kdone = globaltimer();
       if (i == j) {
-        // stages are idle until the next task: use the last one as scratch
         // the whole stage area is idle until the next task: augmented panel + D^-T
         potrf_blocked_tile(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
                            d.LinvT + (size_t)j * TILE, j, d.info, wr, wc, lane);
+      } else if (i == j + 1 && !rhs) {
+        // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
+        acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
       } else {
         double* scratch = sm.slot(last, 0);
         cons_sync();  // every warp has finished reading stage `last`
@@ -573,98 +527,193 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
   }
 }
 
-// u = L^-T y: x_j^T = (y_j^T - sum_{i>j} x_i^T L_ij) inv(L_jj). CTA b handles
-// block j = N-1-b and only waits on lower CTA indices.
-// The critical chain per block is flag -> L_{j+1,j} GEMV -> inv(L_jj) GEMV ->
-// flag, so both tiles are prefetched into shared memory at launch and the
-// post-flag work never touches global memory. The other L_ij contributions
-// are accumulated while later blocks are still being solved.
-constexpr int BW_LDS = 65;  // padded row stride of the prefetched tiles (bank-conflict free column reads)
-__global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, int* __restrict__ xflags,
-                                                        double* __restrict__ xrows /* N*3*64 */,
+// u = L^-T y, block rows from the bottom: x_j = (y_j - sum_{i>j} x_i L_ij) W_j
+// with W_j = inv(L_jj)^T (x_j, y_j: 3 x 64 row blocks; x_i L_ij: 3x64 * 64x64).
+// CTA b owns block j = N-1-b and only waits on lower CTA indices.
+// The chain step j+1 -> j is cut to one small GEMV: at launch every CTA
+// precomputes M_j = L_{j+1,j} W_j in shared memory and prefetches L_{j+2,j};
+// the contributions of x_i, i >= j+2, and c_j = (y_j - sum_{i>=j+2} x_i L_ij) W_j
+// are formed while x_{j+1} is still being solved, so after it arrives only
+// x_j = c_j - x_{j+1} M_j (3 x 64 x 64, split 4 ways + fixed-order reduce) remains.
+// No flags: xrows is preset to an all-ones NaN that arithmetic never produces
+// (results are canonicalised), producers store each value with a relaxed
+// store and one consumer warp polls the 192 values themselves, so a chain
+// step costs one store -> load visibility instead of store, fence, release
+// flag, poll, acquire and reload.
+constexpr int BW_LDS = 65;  // padded row stride of the shared tiles (conflict-free column access)
+constexpr int BW_SMEM_DOUBLES = 4 * TS * BW_LDS + 6 * TS + 12 * TS + 3 * TS + 1;
+constexpr unsigned long long BW_EMPTY = ~0ull;  // sentinel (negative NaN, all payload bits set)
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// warp 0 waits until block i of xrows is complete and stages it in xi
+// (3 x 64); with `also` >= 0 it also stages block `also` into xi + 192 if that
+// one is complete by then. Returns (to every thread) how many were staged.
+__device__ __forceinline__ int bw_fetch(const double* xrows, int i, double* xi, int also, int* nflag) {
+  if (threadIdx.x < 32) {
+    const double* src = xrows + (size_t)i * 3 * TS;
+    const double* src2 = xrows + (size_t)(also >= 0 ? also : i) * 3 * TS;
+    unsigned long long v[6], w[6];
+    bool ready, ready2;
+    do {
+      ready = ready2 = true;
+#pragma unroll
+      for (int e = 0; e < 6; ++e) {
+        v[e] = ld_relaxed_u64(src + threadIdx.x + 32 * e);
+        w[e] = ld_relaxed_u64(src2 + threadIdx.x + 32 * e);
+        ready &= (v[e] != BW_EMPTY);
+        ready2 &= (w[e] != BW_EMPTY);
+      }
+    } while (!__all_sync(0xffffffffu, ready));
+    const bool two = also >= 0 && __all_sync(0xffffffffu, ready2);
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      xi[threadIdx.x + 32 * e] = __longlong_as_double((long long)v[e]);
+      if (two) xi[3 * TS + threadIdx.x + 32 * e] = __longlong_as_double((long long)w[e]);
+    }
+    if (threadIdx.x == 0) *nflag = two ? 2 : 1;
+  }
+  __syncthreads();
+  return *nflag;
+}
+
+// part[grp][r][c] = sum_{k in group} x[r][k] T[k][c]   (T plain, stride BW_LDS)
+__device__ __forceinline__ void bw_gemv_part(const double* x, const double* T, double* part, int c, int grp) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+  for (int k = grp * 16; k < grp * 16 + 16; ++k) {
+    const double l = T[k * BW_LDS + c];
+    a0 += x[k] * l;
+    a1 += x[TS + k] * l;
+    a2 += x[2 * TS + k] * l;
+  }
+  part[(grp * 3 + 0) * TS + c] = a0;
+  part[(grp * 3 + 1) * TS + c] = a1;
+  part[(grp * 3 + 2) * TS + c] = a2;
+}
+__device__ __forceinline__ double bw_reduce(const double* part, int tid) {
+  const int r = tid >> 6, c = tid & 63;
+  return ((part[(0 * 3 + r) * TS + c] + part[(1 * 3 + r) * TS + c]) + part[(2 * 3 + r) * TS + c]) +
+         part[(3 * 3 + r) * TS + c];
+}
+
+__global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __restrict__ xrows /* N*3*64 */,
                                                         double* __restrict__ u, int m) {
   extern __shared__ double bw_sm[];
-  double* sLnext = bw_sm;                 // L_{j+1,j}, plain rows (k, c) at k*BW_LDS + c
-  double* sLiT = bw_sm + TS * BW_LDS;     // LinvT_j: row c holds column c of inv(L_jj)
-  double* xi = sLiT + TS * BW_LDS;        // 3 x 64
-  double* part = xi + 3 * TS;             // 4 x 3 x 64 partial sums
+  double* sW = bw_sm;                   // W[k][c] = inv(L_jj)[c][k]
+  double* sM = sW + TS * BW_LDS;        // M = L_{j+1,j} W
+  double* sL1 = sM + TS * BW_LDS;       // L_{j+1,j} (plain rows)
+  double* sL2 = sL1 + TS * BW_LDS;      // L_{j+2,j}
+  double* xi = sL2 + TS * BW_LDS;       // 2 x 3 x 64
+  double* part = xi + 6 * TS;           // 4 x 3 x 64 partial sums
+  double* cj = part + 12 * TS;          // 3 x 64
+  int* nflag = reinterpret_cast<int*>(cj + 3 * TS);
   const int N = d.N;
   const int j = N - 1 - blockIdx.x;
   const int tid = threadIdx.x;
   const int c = tid & 63, grp = tid >> 6;  // 4 groups x 64 columns
-  // prefetch (plain layout) the two tiles of the critical step
+  // ---- prologue (off the chain): W, L_{j+1,j}, L_{j+2,j} -> smem; M = L_{j+1,j} W
   for (int q = tid; q < TILE; q += 256) {
     const int k = q >> 6, cc = q & 63;
-    if (j + 1 < N) sLnext[k * BW_LDS + cc] = d.L[(size_t)tidx(j + 1, j) * TILE + swz(k, cc)];
-    sLiT[k * BW_LDS + cc] = d.LinvT[(size_t)j * TILE + swz(k, cc)];
+    sW[cc * BW_LDS + k] = d.LinvT[(size_t)j * TILE + swz(k, cc)];  // LinvT row k = column k of inv(L_jj)
+    if (j + 1 < N) sL1[k * BW_LDS + cc] = d.L[(size_t)tidx(j + 1, j) * TILE + swz(k, cc)];
+    if (j + 2 < N) sL2[k * BW_LDS + cc] = d.L[(size_t)tidx(j + 2, j) * TILE + swz(k, cc)];
   }
-  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;  // thread (grp, c): rows k in [16 grp, 16 grp + 16)
-  for (int i = N - 1; i > j; --i) {
-    if (tid == 0) {
-      while (ld_relaxed(xflags + i) == 0) {
-      }
-      fence_acq_rel_gpu();
+  __syncthreads();
+  if (j + 1 < N) {
+    // M[k][c] = sum_p L1[k][p] W[p][c]: thread (grp, c) forms rows k = grp + 4 q
+#pragma unroll 1
+    for (int q = 0; q < 16; ++q) {
+      const int k = grp + 4 * q;
+      double s = 0.0;
+#pragma unroll 16
+      for (int p = 0; p < TS; ++p) s = fma(sL1[k * BW_LDS + p], sW[p * BW_LDS + c], s);
+      sM[k * BW_LDS + c] = s;
     }
-    __syncthreads();
-    if (tid < 3 * TS) xi[tid] = __ldcg(xrows + (size_t)i * 3 * TS + tid);
-    __syncthreads();
-    if (i == j + 1) {
+  }
+  // ---- contributions of x_i, i >= j+3, from the global tiles: the next two
+  // tiles are loaded into registers ahead of their x, and when this CTA is
+  // behind the solved frontier it consumes two ready blocks per round
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+  auto load_tile = [&](int i, double (&t)[16]) {
+    const double* L = d.L + (size_t)tidx(i, j) * TILE;
 #pragma unroll
-      for (int k = grp * 16; k < grp * 16 + 16; ++k) {
-        const double l = sLnext[k * BW_LDS + c];
-        acc0 += xi[k] * l;
-        acc1 += xi[TS + k] * l;
-        acc2 += xi[2 * TS + k] * l;
-      }
-    } else {
-      const double* L = d.L + (size_t)tidx(i, j) * TILE;
+    for (int q = 0; q < 16; ++q) t[q] = L[swz(grp * 16 + q, c)];
+  };
+  auto consume = [&](const double* x, const double (&t)[16]) {
 #pragma unroll
-      for (int k = grp * 16; k < grp * 16 + 16; ++k) {
-        const double l = L[swz(k, c)];
-        acc0 += xi[k] * l;
-        acc1 += xi[TS + k] * l;
-        acc2 += xi[2 * TS + k] * l;
-      }
+    for (int q = 0; q < 16; ++q) {
+      const int k = grp * 16 + q;
+      acc0 += x[k] * t[q];
+      acc1 += x[TS + k] * t[q];
+      acc2 += x[2 * TS + k] * t[q];
     }
-    __syncthreads();
+  };
+  {
+    double ta[16], tb[16];
+    int i = N - 1;
+    if (i >= j + 3) load_tile(i, ta);
+    if (i - 1 >= j + 3) load_tile(i - 1, tb);
+    while (i >= j + 3) {
+      const int got = bw_fetch(xrows, i, xi, i - 1 >= j + 3 ? i - 1 : -1, nflag);
+      consume(xi, ta);
+      if (got == 2) {
+        consume(xi + 3 * TS, tb);
+        if (i - 2 >= j + 3) load_tile(i - 2, ta);
+        if (i - 3 >= j + 3) load_tile(i - 3, tb);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) ta[q] = tb[q];
+        if (i - 2 >= j + 3) load_tile(i - 2, tb);
+      }
+      i -= got;
+      __syncthreads();
+    }
+  }
+  // ---- x_{j+2} from the prefetched tile, then c_j = (y_j - acc) W
+  if (j + 2 < N) {
+    bw_fetch(xrows, j + 2, xi, -1, nflag);
+#pragma unroll
+    for (int k = grp * 16; k < grp * 16 + 16; ++k) {
+      const double l = sL2[k * BW_LDS + c];
+      acc0 += xi[k] * l;
+      acc1 += xi[TS + k] * l;
+      acc2 += xi[2 * TS + k] * l;
+    }
   }
   part[(grp * 3 + 0) * TS + c] = acc0;
   part[(grp * 3 + 1) * TS + c] = acc1;
   part[(grp * 3 + 2) * TS + c] = acc2;
   __syncthreads();
-  if (tid < 3 * TS) {
-    const int r = tid >> 6;
-    const double s = ((part[(0 * 3 + r) * TS + c] + part[(1 * 3 + r) * TS + c]) + part[(2 * 3 + r) * TS + c]) +
-                     part[(3 * 3 + r) * TS + c];
-    xi[tid] = d.Y[(size_t)j * TILE + swz(r, c)] - s;  // tmp = y_j - sum_i x_i L_ij
-  }
+  if (tid < 3 * TS) xi[tid] = d.Y[(size_t)j * TILE + swz(tid >> 6, c)] - bw_reduce(part, tid);
   __syncthreads();
-  // x_j[r][c] = sum_k tmp[r][k] inv(L_jj)[k][c] = sum_k tmp[r][k] LinvT[c][k]
-  {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-    for (int k = grp * 16; k < grp * 16 + 16; ++k) {
-      const double l = sLiT[c * BW_LDS + k];
-      a0 += xi[k] * l;
-      a1 += xi[TS + k] * l;
-      a2 += xi[2 * TS + k] * l;
-    }
-    part[(grp * 3 + 0) * TS + c] = a0;
-    part[(grp * 3 + 1) * TS + c] = a1;
-    part[(grp * 3 + 2) * TS + c] = a2;
-  }
+  bw_gemv_part(xi, sW, part, c, grp);
   __syncthreads();
+  if (tid < 3 * TS) cj[tid] = bw_reduce(part, tid);
+  // ---- the chain step: x_j = c_j - x_{j+1} M
+  double x = 0.0;
+  if (j + 1 < N) {
+    __syncthreads();  // cj complete; xi free
+    bw_fetch(xrows, j + 1, xi, -1, nflag);
+    bw_gemv_part(xi, sM, part, c, grp);
+    __syncthreads();
+    if (tid < 3 * TS) x = cj[tid] - bw_reduce(part, tid);
+  } else if (tid < 3 * TS) {
+    x = cj[tid];
+  }
   if (tid < 3 * TS) {
-    const int r = tid >> 6;
-    const double s = ((part[(0 * 3 + r) * TS + c] + part[(1 * 3 + r) * TS + c]) + part[(2 * 3 + r) * TS + c]) +
-                     part[(3 * 3 + r) * TS + c];
-    xrows[(size_t)j * 3 * TS + r * TS + c] = s;
+    if (isnan(x)) x = CUDART_NAN;  // canonical: never the sentinel
+    st_relaxed_f64(xrows + (size_t)j * 3 * TS + tid, x);
     const int row = j * TS + c;
-    if (row < m) u[3 * row + r] = s;
+    if (row < m) u[3 * row + (tid >> 6)] = x;
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) st_release(xflags + j, 1);
 }
 
 // sigma0 u: per lower tile, the row and (off-diagonal) column contributions.
@@ -746,14 +795,15 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
   k_cholesky_tiles<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
 }
 
-void launch_dense_backward(cudaStream_t st, const DenseDev& d, int* xflags, double* xrows, double* u) {
+void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u) {
   static bool attr = false;
-  const size_t smem = sizeof(double) * (2 * TS * BW_LDS + 3 * TS + 12 * TS);
+  const size_t smem = sizeof(double) * BW_SMEM_DOUBLES;
   if (!attr) {
     cudaFuncSetAttribute(k_dense_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_dense_backward<<<d.N, 256, smem, st>>>(d, xflags, xrows, u, d.m);
+  cudaMemsetAsync(xrows, 0xff, sizeof(double) * 3 * TS * (size_t)d.N, st);  // BW_EMPTY everywhere
+  k_dense_backward<<<d.N, 256, smem, st>>>(d, xrows, u, d.m);
 }
 
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial) {
@@ -764,21 +814,27 @@ void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const doubl
   k_sym_gemv_reduce<<<d.N, 192, 0, st>>>(d, partial, out);
 }
 
-// Task order: column-major (diag, below-diagonal tiles, RHS row), with each
-// diagonal task claimed `lead` columns ahead of its column so its long serial
-// accumulation overlaps the preceding columns. At most lead+1 claimed tasks
-// wait on unclaimed ones, so any grid larger than lead+1 CTAs (or holding all
-// tasks) cannot deadlock.
+// Task order: column-major (below-diagonal tiles, RHS row), with diagonal
+// task d and the partial sum of its sub-diagonal tile (d, d-1) claimed
+// `lead` columns ahead (optionally growing as lead + d / ldiv). A sweep on
+// cfg3 (tools/chol_sweep.sh) found a fixed lead of 1-2 best (2.93 ms); a lead
+// growing with d claims CTAs that then stall in the throughput-bound middle.
+// At most 2 (lead + N / ldiv + 1) claimed tasks wait on unclaimed ones, far
+// below the 148-CTA grid, so the order cannot deadlock.
 std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead) {
-  if (const char* e = getenv("SPB_CHOL_LEAD")) lead = atoi(e);  // diagnostics override
+  int ldiv = 1 << 30, pmode = 0;
+  if (const char* e = getenv("SPB_CHOL_LEAD")) lead = atoi(e);  // diagnostics overrides
+  if (const char* e = getenv("SPB_CHOL_LDIV")) ldiv = std::max(1, atoi(e));
+  if (const char* e = getenv("SPB_CHOL_PMODE")) pmode = atoi(e);  // 1: partial heads its column
   std::vector<int2> tk;
   int next_diag = 0;
   for (int j = 0; j < N; ++j) {
-    while (next_diag < N && next_diag <= j + lead) {
+    while (next_diag < N && next_diag - (lead + next_diag / ldiv) <= j) {
+      if (next_diag > 0 && pmode == 0) tk.push_back(make_int2(next_diag, next_diag - 1));  // partial (d, d-1)
       tk.push_back(make_int2(next_diag, next_diag));
       ++next_diag;
     }
-    // (j+1, j) is produced by the fused diagonal task j+1
+    if (pmode == 1 && j + 1 < N) tk.push_back(make_int2(j + 1, j));
     for (int i = j + 2; i < N; ++i) tk.push_back(make_int2(i, j));
     if (with_rhs) tk.push_back(make_int2(N, j));
   }

@@ -350,7 +350,6 @@ int32_t spb_op_dense_solve(int64_t m, const double* chol, int64_t nrhs, const do
   TMP(int, dflags, nt + N);
   TMP(int, dcnt, 1);
   TMP(int, dinfo, 1);
-  TMP(int, xflags, N);
   TMP(double, xrows, (size_t)N * 3 * 64);
   TMP(double, du, 3 * m);
   std::vector<int2> tk;
@@ -358,7 +357,7 @@ int32_t spb_op_dense_solve(int64_t m, const double* chol, int64_t nrhs, const do
   TMP(int2, dtk, tk.size());
   H2D(dtk.p, tk.data(), sizeof(int2) * tk.size());
   std::vector<int> ready(nt + N, 0);
-  for (int t = 0; t < nt; ++t) ready[t] = 1;
+  for (int t = 0; t < nt; ++t) ready[t] = 2;  // final (sub-diagonal tiles need 2)
   DenseDev d{(int)m, N, nullptr, dL.p, dLi.p, dY.p, dflags.p, dcnt.p, dinfo.p, nullptr, nullptr, nullptr, nullptr,
              nullptr, nullptr, nullptr};
   std::vector<double> ytile((size_t)N * 4096);
@@ -371,9 +370,8 @@ int32_t spb_op_dense_solve(int64_t m, const double* chol, int64_t nrhs, const do
     H2D(dY.p, ytile.data(), sizeof(double) * ytile.size());
     H2D(dflags.p, ready.data(), sizeof(int) * ready.size());
     SPB_CUDA(cudaMemset(dcnt.p, 0, sizeof(int)));
-    SPB_CUDA(cudaMemset(xflags.p, 0, sizeof(int) * N));
     launch_cholesky_tiles(0, d, dtk.p, (int)tk.size(), std::min<int>(NUM_SMS_B200, N));
-    launch_dense_backward(0, d, xflags.p, xrows.p, du.p);
+    launch_dense_backward(0, d, xrows.p, du.p);
     SPB_CUDA(cudaGetLastError());
     D2H(u.data(), du.p, sizeof(double) * 3 * m);
     for (int64_t r = 0; r < m; ++r)

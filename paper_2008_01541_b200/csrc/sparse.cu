@@ -58,12 +58,22 @@ struct DeviceFactor {
   int4* bw_chunks = nullptr;  // (s, c0, first slot, ntiles)
   double* P = nullptr;        // backward tile partials
   int* bw_warp = nullptr;     // s
+  // bottom subtrees (levels < fuse): one CTA per group walks its supernodes
+  // level by level (gather, GEMV) with block barriers instead of launches
+  int fuse = 0, ngroups = 0;
+  int* sub_pos = nullptr;     // struct positions, [group][level] ranges
+  int* sub_pos_off = nullptr; // ngroups * fuse + 1
+  int2* sub_fw = nullptr;     // forward warp tasks (s, r0)
+  int* sub_fw_off = nullptr;
+  int2* sub_bw = nullptr;     // backward warp tasks (s, c0), 8 columns each
+  int* sub_bw_off = nullptr;
   std::vector<LevelTasks> lv;
   std::vector<int> bwt_off, bwr_off, bww_off;  // backward tile / chunk / warp offsets per level
   ~DeviceFactor() {
     for (void* p : {(void*)sn, (void*)rows, (void*)pos_owner, (void*)lvl_pos, (void*)M, (void*)VZ,
                     (void*)asm_ptr, (void*)asm_src, (void*)x2_ptr, (void*)x2_src, (void*)fw_cta, (void*)fw_warp,
-                    (void*)bw_tiles, (void*)bw_chunks, (void*)P, (void*)bw_warp})
+                    (void*)bw_tiles, (void*)bw_chunks, (void*)P, (void*)bw_warp, (void*)sub_pos,
+                    (void*)sub_pos_off, (void*)sub_fw, (void*)sub_fw_off, (void*)sub_bw, (void*)sub_bw_off})
       if (p) cudaFree(p);
   }
 };
@@ -352,6 +362,194 @@ __global__ void __launch_bounds__(256) k_backward_warp(const SnDev* __restrict__
   }
 }
 
+// ------------------------------------------------- bottom-subtree kernels
+// The lower elimination-tree levels hold thousands of small supernodes
+// (cfg3: levels 0-6 = 5.5K supernodes, 105 MB of panels) whose per-level
+// launches are latency-bound. Whole subtrees are grouped (balanced by panel
+// bytes) and one CTA per group runs all those levels, with block barriers
+// between the dependent steps; the children's updates and the ancestors' x are
+// produced by the same CTA (or by the level kernels before/after the launch).
+constexpr int SUB_THREADS = 512;
+constexpr int SUB_WARPS = SUB_THREADS / 32;
+constexpr int SUB_BWC = 8;  // backward warp task width (columns)
+
+// One warp: rows r0..r0+31 of M_s times the assembled v (any nc), in column order.
+__device__ __forceinline__ void fw_warp_rows(const SnDev& S, int r0, int lane, const double* __restrict__ M,
+                                             const double* V, double* y, double* U) {
+  const int r = r0 + lane;
+  const bool valid = r < S.nr;
+  const int cmax = (r0 < S.nc) ? min(S.nc, r0 + 32) : S.nc;  // inv(L_ss) is lower triangular
+  const double* Vs = V + 3 * (int64_t)S.rowoff;
+  const double* Mp = M + S.valoff + (valid ? r : 0);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  // 16 independent panel loads in flight per lane (latency-bound otherwise);
+  // the chunk's 48 v entries come in with two coalesced loads and are
+  // broadcast by shuffles (entry e = 3u + q sits in lane e % 32 of load e / 32)
+  for (int c = 0; c < cmax; c += 16) {
+    double mv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) mv[u] = (c + u < cmax) ? Mp[(int64_t)(c + u) * S.nr] : 0.0;
+    const int nv = 3 * min(16, cmax - c);
+    const double vlo = lane < nv ? Vs[3 * c + lane] : 0.0;
+    const double vhi = lane + 32 < nv ? Vs[3 * c + 32 + lane] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const double v0 = (3 * u + 0 < 32) ? __shfl_sync(0xffffffffu, vlo, (3 * u + 0) & 31)
+                                         : __shfl_sync(0xffffffffu, vhi, (3 * u + 0) & 31);
+      const double v1 = (3 * u + 1 < 32) ? __shfl_sync(0xffffffffu, vlo, (3 * u + 1) & 31)
+                                         : __shfl_sync(0xffffffffu, vhi, (3 * u + 1) & 31);
+      const double v2 = (3 * u + 2 < 32) ? __shfl_sync(0xffffffffu, vlo, (3 * u + 2) & 31)
+                                         : __shfl_sync(0xffffffffu, vhi, (3 * u + 2) & 31);
+      if (c + u < cmax) {
+        a0 += mv[u] * v0;
+        a1 += mv[u] * v1;
+        a2 += mv[u] * v2;
+      }
+    }
+  }
+  if (!valid) return;
+  if (r < S.nc) {
+    y[3 * (int64_t)(S.first + r) + 0] = a0;
+    y[3 * (int64_t)(S.first + r) + 1] = a1;
+    y[3 * (int64_t)(S.first + r) + 2] = a2;
+  } else {
+    const int64_t o = 3 * (int64_t)(S.uoff + r - S.nc);
+    U[o + 0] = Vs[3 * r + 0] - a0;
+    U[o + 1] = Vs[3 * r + 1] - a1;
+    U[o + 2] = Vs[3 * r + 2] - a2;
+  }
+}
+
+// lane l ends with the warp total of entry l % 8
+__device__ __forceinline__ double warp_transpose_sum8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 8);
+#pragma unroll
+  for (int off = 4; off >= 1; off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = upper ? v[i] : v[i + off];
+      const double keep = upper ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+__global__ void __launch_bounds__(SUB_THREADS) k_subtree_forward(
+    const SnDev* __restrict__ sn, const double* __restrict__ M, const int* __restrict__ pos,
+    const int* __restrict__ pos_off, const int2* __restrict__ tasks, const int* __restrict__ task_off, int fuse,
+    const int* __restrict__ owner, const int* __restrict__ ap, const int* __restrict__ as,
+    const double* __restrict__ b, double* V, double* y, double* U) {
+  const int g = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = 0; l < fuse; ++l) {
+    const int q0 = pos_off[g * fuse + l], q1 = pos_off[g * fuse + l + 1];
+    for (int t = q0 + (int)threadIdx.x; t < q1; t += SUB_THREADS) {
+      const int p = pos[t];
+      const int o = owner[p];
+      double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+      if (o >= 0) {
+        v0 = b[3 * (int64_t)o + 0];
+        v1 = b[3 * (int64_t)o + 1];
+        v2 = b[3 * (int64_t)o + 2];
+      }
+      for (int k = ap[p]; k < ap[p + 1]; ++k) {
+        const double* u = U + 3 * (int64_t)as[k];
+        v0 += u[0];
+        v1 += u[1];
+        v2 += u[2];
+      }
+      V[3 * (int64_t)p + 0] = v0;
+      V[3 * (int64_t)p + 1] = v1;
+      V[3 * (int64_t)p + 2] = v2;
+    }
+    __syncthreads();
+    const int t0 = task_off[g * fuse + l], t1 = task_off[g * fuse + l + 1];
+    for (int t = t0 + warp; t < t1; t += SUB_WARPS) {
+      const int2 tk = tasks[t];
+      fw_warp_rows(sn[tk.x], tk.y, lane, M, V, y, U);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(SUB_THREADS) k_subtree_backward(
+    const SnDev* __restrict__ sn, const double* __restrict__ M, const int* __restrict__ pos,
+    const int* __restrict__ pos_off, const int2* __restrict__ tasks, const int* __restrict__ task_off, int fuse,
+    const int* __restrict__ owner, const int* __restrict__ rows, const double* __restrict__ y, double* Z,
+    double* XF) {
+  const int g = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int l = fuse - 1; l >= 0; --l) {
+    const int q0 = pos_off[g * fuse + l], q1 = pos_off[g * fuse + l + 1];
+    for (int t = q0 + (int)threadIdx.x; t < q1; t += SUB_THREADS) {
+      const int p = pos[t];
+      const int o = owner[p];
+      double z0, z1, z2;
+      if (o >= 0) {
+        z0 = y[3 * (int64_t)o + 0];
+        z1 = y[3 * (int64_t)o + 1];
+        z2 = y[3 * (int64_t)o + 2];
+      } else {
+        const double* x = XF + 3 * (int64_t)rows[p];
+        z0 = -x[0];
+        z1 = -x[1];
+        z2 = -x[2];
+      }
+      Z[3 * (int64_t)p + 0] = z0;
+      Z[3 * (int64_t)p + 1] = z1;
+      Z[3 * (int64_t)p + 2] = z2;
+    }
+    __syncthreads();
+    const int t0 = task_off[g * fuse + l], t1 = task_off[g * fuse + l + 1];
+    for (int t = t0 + warp; t < t1; t += SUB_WARPS) {
+      const int2 tk = tasks[t];  // (s, c0)
+      const SnDev S = sn[tk.x];
+      const int c0 = tk.y, ncc = min(SUB_BWC, S.nc - c0);
+      const double* Zs = Z + 3 * (int64_t)S.rowoff;
+      const double* Mc = M + S.valoff + (int64_t)c0 * S.nr;
+      double acc[3][SUB_BWC];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int cc = 0; cc < SUB_BWC; ++cc) acc[q][cc] = 0.0;
+      // rows above c0 are zero in the inv(L_ss) block; two row steps per
+      // iteration keep 16 panel loads in flight per lane
+      for (int r = c0 + lane; r < S.nr; r += 64) {
+        double z[2][3], mv[2][SUB_BWC];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int rr = r + 32 * h;
+          const bool ok = rr < S.nr;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) z[h][q] = ok ? Zs[3 * rr + q] : 0.0;
+#pragma unroll
+          for (int cc = 0; cc < SUB_BWC; ++cc) mv[h][cc] = (ok && cc < ncc) ? Mc[(int64_t)cc * S.nr + rr] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int cc = 0; cc < SUB_BWC; ++cc) {
+            acc[0][cc] += mv[h][cc] * z[h][0];
+            acc[1][cc] += mv[h][cc] * z[h][1];
+            acc[2][cc] += mv[h][cc] * z[h][2];
+          }
+      }
+      const double o0 = warp_transpose_sum8(acc[0], lane);
+      const double o1 = warp_transpose_sum8(acc[1], lane);
+      const double o2 = warp_transpose_sum8(acc[2], lane);
+      if (lane < ncc) {
+        XF[3 * (int64_t)(S.first + c0 + lane) + 0] = o0;
+        XF[3 * (int64_t)(S.first + c0 + lane) + 1] = o1;
+        XF[3 * (int64_t)(S.first + c0 + lane) + 2] = o2;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- host
 template <typename T>
 static int upload(T** dst, const std::vector<T>& v) {
@@ -484,6 +682,95 @@ int build_device_factor(Factor& f) {
   d->bwt_off[f.nlevels] = (int)bwt.size();
   d->bwr_off[f.nlevels] = (int)bwr.size();
   d->bww_off[f.nlevels] = (int)bww.size();
+  // ---- bottom subtrees: choose the fuse height f by a small cost model
+  // (slowest group's panel bytes at ~15 GB/s effective per SM + ~20 us per remaining
+  // level launch pair), group whole subtrees (LPT on bytes, 148 groups)
+  {
+    std::vector<std::vector<int64_t>> kids(ns);
+    for (int64_t s = 0; s < ns; ++s)
+      if (f.sn_parent[s] >= 0) kids[f.sn_parent[s]].push_back(s);
+    auto plan = [&](int fz, std::vector<int64_t>& roots, std::vector<std::vector<int64_t>>& members,
+                    std::vector<int>& group_of_root, int& G) -> double {
+      roots.clear();
+      for (int64_t s = 0; s < ns; ++s)
+        if (f.sn_level[s] < fz && (f.sn_parent[s] < 0 || f.sn_level[f.sn_parent[s]] >= fz)) roots.push_back(s);
+      members.assign(roots.size(), {});
+      std::vector<double> work(roots.size(), 0.0);
+      for (size_t k = 0; k < roots.size(); ++k) {
+        std::vector<int64_t> stack{roots[k]};
+        while (!stack.empty()) {
+          int64_t s = stack.back();
+          stack.pop_back();
+          members[k].push_back(s);
+          work[k] += (double)sn[s].nc * sn[s].nr;
+          for (int64_t c : kids[s]) stack.push_back(c);
+        }
+      }
+      G = (int)std::min<size_t>(NUM_SMS_B200, roots.size());
+      group_of_root.assign(roots.size(), 0);
+      if (G == 0) return 1e30;
+      std::vector<size_t> ord(roots.size());
+      for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
+      std::stable_sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return work[a] > work[b]; });
+      std::vector<double> load(G, 0.0);
+      for (size_t k : ord) {
+        int gmin = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[gmin] += work[k];
+        group_of_root[k] = gmin;
+      }
+      const double maxb = 8.0 * *std::max_element(load.begin(), load.end());
+      return maxb / 15e9 + 20e-6 * (double)(f.nlevels - fz);
+    };
+    int best = 0;
+    double best_t = 20e-6 * (double)f.nlevels;
+    std::vector<int64_t> roots;
+    std::vector<std::vector<int64_t>> members;
+    std::vector<int> gor;
+    int G = 0;
+    const char* env = getenv("SPB_SWEEP_FUSE");
+    if (env) {
+      best = std::max(0, std::min((int)f.nlevels, atoi(env)));
+    } else {
+      for (int fz = 1; fz <= (int)f.nlevels; ++fz) {
+        const double t = plan(fz, roots, members, gor, G);
+        if (t < best_t) best_t = t, best = fz;
+      }
+    }
+    d->fuse = best;
+    if (best > 0) plan(best, roots, members, gor, G);
+    d->ngroups = best > 0 ? G : 0;
+    std::vector<int> spos, spos_off, sfw_off, sbw_off;
+    std::vector<int2> sfw, sbw;
+    if (best > 0) {
+      std::vector<std::vector<std::vector<int64_t>>> byg(G, std::vector<std::vector<int64_t>>(best));
+      for (size_t k = 0; k < roots.size(); ++k)
+        for (int64_t s : members[k]) byg[gor[k]][f.sn_level[s]].push_back(s);
+      for (int g = 0; g < G; ++g)
+        for (int l = 0; l < best; ++l) {
+          auto& v = byg[g][l];
+          std::sort(v.begin(), v.end());
+          spos_off.push_back((int)spos.size());
+          sfw_off.push_back((int)sfw.size());
+          sbw_off.push_back((int)sbw.size());
+          for (int64_t s : v) {
+            const SnDev& S = sn[s];
+            for (int k = 0; k < S.nr; ++k) spos.push_back(S.rowoff + k);
+            for (int r0 = 0; r0 < S.nr; r0 += 32) sfw.push_back(make_int2((int)s, r0));
+            for (int c0 = 0; c0 < S.nc; c0 += SUB_BWC) sbw.push_back(make_int2((int)s, c0));
+          }
+        }
+      spos_off.push_back((int)spos.size());
+      sfw_off.push_back((int)sfw.size());
+      sbw_off.push_back((int)sbw.size());
+    }
+    int rc2;
+    if ((rc2 = upload(&d->sub_pos, spos)) || (rc2 = upload(&d->sub_pos_off, spos_off)) ||
+        (rc2 = upload(&d->sub_fw, sfw)) || (rc2 = upload(&d->sub_fw_off, sfw_off)) ||
+        (rc2 = upload(&d->sub_bw, sbw)) || (rc2 = upload(&d->sub_bw_off, sbw_off))) {
+      delete d;
+      return rc2;
+    }
+  }
   int rc;
   if ((rc = upload(&d->sn, sn)) || (rc = upload(&d->rows, rows)) || (rc = upload(&d->pos_owner, owner)) ||
       (rc = upload(&d->lvl_pos, lpos)) || (rc = upload(&d->M, f.Mval)) || (rc = upload(&d->asm_ptr, cnt)) ||
@@ -511,7 +798,13 @@ int build_device_factor(Factor& f) {
 
 void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
                     int* launches) {
-  for (int l = 0; l < d.nlevels; ++l) {
+  if (d.fuse > 0) {
+    k_subtree_forward<<<d.ngroups, SUB_THREADS, 0, st>>>(d.sn, d.M, d.sub_pos, d.sub_pos_off, d.sub_fw,
+                                                         d.sub_fw_off, d.fuse, d.pos_owner, d.asm_ptr, d.asm_src, b,
+                                                         d.VZ, y, U);
+    if (launches) ++*launches;
+  }
+  for (int l = d.fuse; l < d.nlevels; ++l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
     k_fw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.asm_ptr,
@@ -530,7 +823,7 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
 }
 
 void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches) {
-  for (int l = d.nlevels - 1; l >= 0; --l) {
+  for (int l = d.nlevels - 1; l >= d.fuse; --l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
     k_bw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.rows, y, XF,
@@ -545,6 +838,11 @@ void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, do
     }
     if (nw) k_backward_warp<<<(nw + 7) / 8, 256, 0, st>>>(d.sn, d.M, d.VZ, d.bw_warp + d.bww_off[l], nw, XF);
     if (launches) *launches += 1 + 2 * (nt > 0) + (nw > 0);
+  }
+  if (d.fuse > 0) {
+    k_subtree_backward<<<d.ngroups, SUB_THREADS, 0, st>>>(d.sn, d.M, d.sub_pos, d.sub_pos_off, d.sub_bw,
+                                                          d.sub_bw_off, d.fuse, d.pos_owner, d.rows, y, d.VZ, XF);
+    if (launches) ++*launches;
   }
 }
 

@@ -42,7 +42,7 @@ def test_cfg3_three_step_solve_equals_monolithic(cfg3):
     y1, ft2 = P.forward_sub(f, b1, b2)
     x2 = P.dense_solve(P.dense_factor(np.asarray(f.sigma0)), ft2)
     x1 = P.backward_sub(f, y1, x2)
-    A = cfg3.system.A
+    A = cfg3.system.A.full()
     x = np.concatenate([x1, x2])
     b = np.concatenate([b1, b2])
     assert np.linalg.norm(A @ x - b) <= 1e-10 * np.linalg.norm(b)

@@ -30,11 +30,13 @@ tail = [done[(j, j)] - fin[(j, j)] for j in range(N)]
 print("diag: compute (kdone->fin) mean %.2f us, tail (fin->released) mean %.2f us" % (np.mean(pc), np.mean(tail)))
 offt = [row[2] - row[3] for (i, j), row in zip(tk, T) if i != j]
 print("offdiag tail mean %.2f us" % np.mean(offt))
-print(" j  claim  kdone  fdone | potrf  trsm(j+1,j)  diag_wait_lastk")
+print(" j  claim  kdone  fdone | potrf  gap(diag j -> potrf j+1)  kdone-after-partial")
 rows = []
 for j in range(N):
     pot = done[(j, j)] - kd[(j, j)]
-    trsm = done[(j + 1, j)] - done[(j, j)] if (j + 1, j) in done else float("nan")
+    # gap: diag j-1 released -> diag j starts its factorization (includes the
+    # sub-diagonal finalize + rank-64 update done inside diag task j)
+    trsm = kd[(j + 1, j + 1)] - done[(j, j)] if (j + 1, j + 1) in kd else float("nan")
     wait = kd[(j, j)] - done.get((j, j - 1), float("nan")) if j > 0 else float("nan")
     rows.append((pot, trsm, wait))
     if j % 8 == 0 or j == N - 1:
