@@ -70,6 +70,11 @@ typedef struct spb_ctx spb_ctx;
 int32_t spb_version(void);
 const char *spb_last_error(void);
 int32_t spb_device_count(int32_t *count);
+/* Page-lock a caller-owned host range so spb_ctx_set_state / get_state move
+ * it by DMA without staging (e.g. a SolverState.x reused every frame); the
+ * caller unregisters it before freeing the memory. */
+int32_t spb_host_register(void *ptr, int64_t bytes);
+int32_t spb_host_unregister(void *ptr);
 
 /* ----------------------------------------------------------- precompute */
 

@@ -9,6 +9,7 @@ missing, calls raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 import subprocess
 from pathlib import Path
@@ -74,6 +75,8 @@ _SIGS = {
     "spb_version": ([], I32),
     "spb_last_error": ([], ctypes.c_char_p),
     "spb_device_count": ([P], I32),
+    "spb_host_register": ([P, I64], I32),
+    "spb_host_unregister": ([P], I32),
     "spb_set_host_blas": ([P, P, P, P, P], I32),
     "spb_factor_create": ([I64, I64, P, P, P, P, I32, I32, P, P], I32),
     "spb_factor_destroy": ([P], None),
@@ -191,6 +194,43 @@ def f64(a, shape=None) -> np.ndarray:
 
 def i64(a) -> np.ndarray:
     return np.ascontiguousarray(a, dtype=np.int64)
+
+
+# ---------------------------------------------------------- pinned reuse
+_pinned: dict = {}  # data pointer -> weakref.finalize of the owning array
+_seen: dict = {}    # data pointer -> id of the owning array at first sighting
+
+
+def _unpin(ptr: int) -> None:
+    _pinned.pop(ptr, None)
+    if _lib is not None:
+        _lib.spb_host_unregister(ctypes.c_void_p(ptr))
+
+
+def pin_reused(arr: np.ndarray, min_bytes: int = 1 << 20) -> None:
+    """Page-lock `arr`'s buffer in place the second time the same buffer is
+    handed to the device path (a SolverState.x stepped frame after frame), so
+    its upload/download is a direct DMA instead of a staged copy. The
+    registration is dropped (finalizer on the owning array) before numpy frees
+    the memory."""
+    if not (isinstance(arr, np.ndarray) and arr.flags.c_contiguous and arr.nbytes >= min_bytes):
+        return
+    ptr = arr.ctypes.data
+    if ptr in _pinned:
+        return
+    root = arr
+    while isinstance(root.base, np.ndarray):
+        root = root.base
+    if root.base is not None or root.ctypes.data != ptr or root.nbytes != arr.nbytes:
+        return  # memory owned elsewhere, or a sub-range: leave it to the staging path
+    if _seen.get(ptr) != id(root):
+        if len(_seen) > 64:
+            _seen.clear()
+        _seen[ptr] = id(root)
+        return
+    if lib().spb_host_register(ctypes.c_void_p(ptr), arr.nbytes) != SPB_OK:
+        return
+    _pinned[ptr] = weakref.finalize(root, _unpin, ptr)
 
 
 def device_count() -> int:

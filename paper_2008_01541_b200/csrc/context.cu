@@ -195,27 +195,51 @@ struct IoList {
   }
 };
 
+// Host buffers the caller page-locked (spb_host_register) are copied by DMA
+// directly; everything else goes through the staging area.
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static int io_upload(Ctx* c, const IoList& l) {
   TRY(c->io_reserve(l.total));
   size_t off = 0;
   for (int i = 0; i < l.n; ++i) {
+    if (host_pinned(l.items[i].host)) {
+      SPB_CUDA(cudaMemcpyAsync(l.items[i].dev, l.items[i].host, l.items[i].bytes, cudaMemcpyHostToDevice, c->st));
+      continue;
+    }
     memcpy(c->io_host + off, l.items[i].host, l.items[i].bytes);
     SPB_CUDA(cudaMemcpyAsync(l.items[i].dev, c->io_host + off, l.items[i].bytes, cudaMemcpyHostToDevice, c->st));
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
+  // the caller may reuse its buffers as soon as we return
+  SPB_CUDA(cudaStreamSynchronize(c->st));
   return SPB_OK;
 }
 
 static int io_download(Ctx* c, const IoList& l) {
   TRY(c->io_reserve(l.total));
   size_t off = 0;
+  bool staged[8] = {};
   for (int i = 0; i < l.n; ++i) {
+    if (host_pinned(l.items[i].host)) {
+      SPB_CUDA(cudaMemcpyAsync(l.items[i].host, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, c->st));
+      continue;
+    }
+    staged[i] = true;
     SPB_CUDA(cudaMemcpyAsync(c->io_host + off, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, c->st));
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
   SPB_CUDA(cudaStreamSynchronize(c->st));
   off = 0;
   for (int i = 0; i < l.n; ++i) {
+    if (!staged[i]) continue;
     memcpy(l.items[i].host, c->io_host + off, l.items[i].bytes);
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
@@ -513,6 +537,21 @@ using spb::io_download;
 extern "C" {
 
 int32_t spb_version(void) { return 100; }
+
+int32_t spb_host_register(void* p, int64_t bytes) {
+  SPB_GUARD_BEGIN
+  if (!p || bytes <= 0) { spb::set_error("null/empty host range"); return SPB_ERR_ARG; }
+  SPB_CUDA(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_host_unregister(void* p) {
+  SPB_GUARD_BEGIN
+  SPB_CUDA(cudaHostUnregister(p));
+  return SPB_OK;
+  SPB_GUARD_END
+}
 const char* spb_last_error(void) { return spb::g_last_error.c_str(); }
 int32_t spb_device_count(int32_t* count) {
   int c = 0;
