@@ -244,10 +244,20 @@ constexpr int LDT = 20;        // row stride of the 16 x 16 D^-T block
 __device__ __forceinline__ double pivot_rsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y;
+  // one third-order correction, y (1 + e/2 + 3 e^2 / 8) with e = 1 - x y^2:
+  // relative error O(e^3) from the ~2^-22 approximation (4 dependent ops
+  // instead of the 6 of two Newton steps)
+  const double e = fma(-(x * y), y, 1.0);
+  const double p = fma(e, 0.375, 0.5);
+  return fma(y * e, p, y);
+}
+
+// double shuffle as two explicit 32-bit shuffles (the generic overload makes
+// the register allocator shuffle the halves around with XOR swaps)
+__device__ __forceinline__ double shfl_f64(double v, int src) {
+  const int lo = __shfl_sync(0xffffffffu, __double2loint(v), src);
+  const int hi = __shfl_sync(0xffffffffu, __double2hiint(v), src);
+  return __hiloint2double(hi, lo);
 }
 
 __device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j, int* info, int lane) {
@@ -257,20 +267,27 @@ __device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j
 #pragma unroll
   for (int c = 0; c < 16; ++c) v[c] = drow ? S[(o + lane) * LSP + o + c] : ((c == lane - 16) ? 1.0 : 0.0);
   int badk = -1;  // first non-positive pivot of the block
+  double dnext = shfl_f64(v[0], 0);
 #pragma unroll 16
   for (int k = 0; k < 16; ++k) {
-    const double dkk = __shfl_sync(0xffffffffu, v[k], k);
+    const double dkk = dnext;
     badk = (badk < 0 && !(dkk > 0.0)) ? k : badk;
     const double ip = pivot_rsqrt(dkk);
     const bool active = lane > k;  // rows below the pivot (all identity lanes)
     const double l = v[k] * ip;
+    // one select per column instead of one per updated entry: rows at or
+    // above the pivot multiply by zero (their entries stay as they are)
+    const double lm = active ? l : 0.0;
     v[k] = (lane == k) ? dkk * ip : (active ? l : v[k]);
+    if (k < 15) {
+      // critical chain first: lane k+1's updated diagonal needs only its own
+      // l (v[k+1] - l^2, bitwise what the shuffled update gives it), so the
+      // next pivot is one shuffle away
+      dnext = shfl_f64(fma(-lm, l, v[k + 1]), k + 1);
+    }
 #pragma unroll 16
     for (int c = 0; c < 16; ++c) {
-      if (c > k) {
-        const double lc = __shfl_sync(0xffffffffu, l, c);
-        v[c] = active ? fma(-l, lc, v[c]) : v[c];
-      }
+      if (c > k) v[c] = fma(-lm, shfl_f64(l, c), v[c]);
     }
   }
   if (badk >= 0 && lane == 0) atomicCAS(info, 0, j * TS + o + badk + 1);
@@ -283,9 +300,50 @@ __device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j
   }
 }
 
+#ifdef SPB_POTRF_PROF  // tools/potrf_bench.cu: per-phase clocks of thread 0
+__device__ long long g_potrf_prof[32];
+#define POTRF_MARK(n) \
+  if (threadIdx.x == 0) g_potrf_prof[n] += clock64();
+#else
+#define POTRF_MARK(n)
+#endif
+
+// rank-16 update of the 8x8 block (rb, cb) of the augmented panel by the
+// factored column block o: S[rb][cb] -= P[rb][o:o+16] P[cb][o:o+16]^T,
+// two blocks per call so their DMMA chains overlap
+__device__ __forceinline__ void upd_block2(double* S, int o, int rbA, int cbA, bool okA, int rbB, int cbB, bool okB,
+                                           int g, int t) {
+  const int rb[2] = {okA ? rbA : 0, okB ? rbB : 0}, cb[2] = {okA ? cbA : 0, okB ? cbB : 0};
+  const bool ok[2] = {okA, okB};
+  double c0[2], c1[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const double* pc = S + (rb[u] * 8 + g) * LSP + cb[u] * 8 + 2 * t;
+    c0[u] = ok[u] ? pc[0] : 0.0;
+    c1[u] = ok[u] ? pc[1] : 0.0;
+  }
+#pragma unroll
+  for (int k0 = 0; k0 < 16; k0 += 4)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      dmma(c0[u], c1[u], -S[(rb[u] * 8 + g) * LSP + o + t + k0], S[(cb[u] * 8 + g) * LSP + o + t + k0]);
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (ok[u]) {
+      double* pc = S + (rb[u] * 8 + g) * LSP + cb[u] * 8 + 2 * t;
+      pc[0] = c0[u];
+      pc[1] = c1[u];
+    }
+}
+
+// Look-ahead blocked factorization: after the panel solve of column block kb,
+// warp 0 updates the next 16x16 diagonal block and factors it right away while
+// warps 1-7 apply the rest of the rank-16 trailing update, so the sequential
+// 16-pivot kernels overlap the update work (2 consumer barriers per block).
 __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
                                    int* info, int wr, int wc, int lane) {
   const int tid = threadIdx.x, warp = tid >> 5;
+  POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
   cons_sync();  // every warp has finished reading the stage area
   acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
@@ -297,14 +355,44 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
     S[(64 + r) * LSP + c] = (r == c) ? 1.0 : 0.0;
   }
   cons_sync();
+  POTRF_MARK(1)
 #pragma unroll 1
   for (int kb = 0; kb < 4; ++kb) {
     const int o = 16 * kb;
-    if (warp == 0) potrf_diag16(S, DT, o, j, info, lane);
+    // (a) the trailing update by column block kb-1 (rows [o, 128) x cols
+    // [o, 64)): warp 0 updates the 16x16 diagonal block of kb and factors it
+    // right away (one call site: the unrolled 16-pivot kernel is large);
+    // warps 1..7 update every other block meanwhile
+    if (warp == 0) {
+      if (kb > 0) {
+        const int d0 = o >> 3;
+        upd_block2(S, o - 16, d0, d0, true, d0 + 1, d0, true, g, t);
+        upd_block2(S, o - 16, d0 + 1, d0 + 1, true, 0, 0, false, g, t);
+        __syncwarp();
+      }
+      potrf_diag16(S, DT, o, j, info, lane);
+    } else if (kb > 0) {
+      const int rb0 = o >> 3, cb0 = rb0, nrb = 16 - rb0, ncb = 8 - cb0;
+      const int nblk = nrb * ncb;
+      for (int b2 = warp - 1; b2 < nblk; b2 += 2 * (NCONS / 32 - 1)) {
+        int rbu[2], cbu[2];
+        bool oku[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int bidx = b2 + u * (NCONS / 32 - 1);
+          rbu[u] = rb0 + bidx / ncb;
+          cbu[u] = cb0 + bidx % ncb;
+          const bool diag = rbu[u] < rb0 + 2 && cbu[u] < cb0 + 2;  // warp 0's
+          oku[u] = bidx < nblk && !diag && !(rbu[u] < 8 && rbu[u] < cbu[u]);  // unused upper blocks
+        }
+        upd_block2(S, o - 16, rbu[0], cbu[0], oku[0], rbu[1], cbu[1], oku[1], g, t);
+      }
+    }
     cons_sync();
-    // panel: rows [o+16, 128) x cols [o, o+16): P = S_panel * D^-T (in place)
-    const int rb0 = (o + 16) >> 3, nrb = 16 - rb0;
-    for (int rb = rb0 + warp; rb < 16; rb += NCONS / 32) {
+    POTRF_MARK(2 + 2 * kb)
+    // (b) panel: rows [o+16, 128) x cols [o, o+16): P = S_panel * D^-T (in place)
+    const int pb0 = (o + 16) >> 3;
+    for (int rb = pb0 + warp; rb < 16; rb += NCONS / 32) {
       double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
       const double* pa = S + (rb * 8 + g) * LSP + o + t;
 #pragma unroll
@@ -320,26 +408,8 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
       pw[8] = c1[0];
       pw[9] = c1[1];
     }
-    (void)nrb;
     cons_sync();
-    // trailing update: S[r][c] -= P[r][:] P[c][:] for c in [o+16, 64), r in [o+16, 128)
-    if (kb < 3) {
-      const int cb0 = (o + 16) >> 3, ncb = 8 - cb0;
-      const int nblk = nrb * ncb;
-      for (int bidx = warp; bidx < nblk; bidx += NCONS / 32) {
-        const int rb = rb0 + bidx / ncb, cb = cb0 + bidx % ncb;
-        if (rb < 8 && rb < cb) continue;  // strictly upper block of the L part: unused
-        double* pc = S + (rb * 8 + g) * LSP + cb * 8 + 2 * t;
-        double c0 = pc[0], c1 = pc[1];
-        const double* pa = S + (rb * 8 + g) * LSP + o + t;
-        const double* pb = S + (cb * 8 + g) * LSP + o + t;
-#pragma unroll
-        for (int k0 = 0; k0 < 16; k0 += 4) dmma(c0, c1, -pa[k0], pb[k0]);
-        pc[0] = c0;
-        pc[1] = c1;
-      }
-      cons_sync();
-    }
+    POTRF_MARK(3 + 2 * kb)
   }
   // L_jj (strict upper zeroed) and L_jj^-T to global (swizzled tiles)
   for (int q = tid; q < 64 * 64; q += NCONS) {
@@ -347,6 +417,7 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
     gL[swz(r, c)] = (c <= r) ? S[r * LSP + c] : 0.0;
     gLinvT[swz(r, c)] = S[(64 + r) * LSP + c];
   }
+  POTRF_MARK(14)
 }
 
 // ---------------------------------------------------------------- kernel

@@ -37,6 +37,7 @@ struct LevelTasks {
   int cta_off, ncta, warp_off, nwarp;
   int pos_off, npos;  // struct positions of the level (gather kernels)
   int max_nc;         // forward CTA tasks: columns staged in smem
+  int rows;           // forward CTA task height (32, 16 or 8: >= ~4 waves per level)
 };
 
 struct DeviceFactor {
@@ -67,13 +68,27 @@ struct DeviceFactor {
   int* sub_fw_off = nullptr;
   int2* sub_bw = nullptr;     // backward warp tasks (s, c0), 8 columns each
   int* sub_bw_off = nullptr;
+  // dataflow sweeps over the levels >= fuse (one persistent launch each)
+  int flow = 0, nft = 0, nbt = 0, nbch = 0;
+  int* parent = nullptr;       // supernode parent or -1
+  int4* ftasks = nullptr;      // (kind 0 gather / 1 rows, s, r0, -)
+  int* f_need = nullptr;       // row tasks of the children a supernode's gather waits for
+  int4* btasks = nullptr;      // gather: (-(s+1), 0, 0, 0); tile: (s, c0, r0, slot)
+  int* btask_chunk = nullptr;  // chunk of a tile task
+  int4* bchunks = nullptr;     // (s, c0, first slot, ntiles)
+  int* b_need = nullptr;       // column chunks of the parent a supernode's gather waits for
+  int* flow_cnt = nullptr;     // counters, zeroed per sweep: [claim | per supernode x 2 | per chunk]
+  int fw_grid = 0, bw_grid = 0;
+  size_t fw_smem = 0;
   std::vector<LevelTasks> lv;
   std::vector<int> bwt_off, bwr_off, bww_off;  // backward tile / chunk / warp offsets per level
   ~DeviceFactor() {
     for (void* p : {(void*)sn, (void*)rows, (void*)pos_owner, (void*)lvl_pos, (void*)M, (void*)VZ,
                     (void*)asm_ptr, (void*)asm_src, (void*)x2_ptr, (void*)x2_src, (void*)fw_cta, (void*)fw_warp,
                     (void*)bw_tiles, (void*)bw_chunks, (void*)P, (void*)bw_warp, (void*)sub_pos,
-                    (void*)sub_pos_off, (void*)sub_fw, (void*)sub_fw_off, (void*)sub_bw, (void*)sub_bw_off})
+                    (void*)sub_pos_off, (void*)sub_fw, (void*)sub_fw_off, (void*)sub_bw, (void*)sub_bw_off,
+                    (void*)parent, (void*)ftasks, (void*)f_need, (void*)btasks, (void*)btask_chunk,
+                    (void*)bchunks, (void*)b_need, (void*)flow_cnt})
       if (p) cudaFree(p);
   }
 };
@@ -149,28 +164,34 @@ __global__ void k_bw_gather(const int* __restrict__ lvl_pos, int npos, const int
 __global__ void __launch_bounds__(FW_THREADS) k_forward_level(const SnDev* __restrict__ sn, const double* __restrict__ M,
                                                        const double* __restrict__ V,
                                                        const int2* __restrict__ cta_tasks, int ncta,
-                                                       const int2* __restrict__ warp_tasks, int nwarp,
+                                                       const int2* __restrict__ warp_tasks, int nwarp, int rows,
                                                        double* __restrict__ y, double* __restrict__ U) {
   extern __shared__ __align__(16) double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if ((int)blockIdx.x < ncta) {
+    // task (s, r0): rows r0..r0+R-1 of M_s; lane = row + R * column group, the
+    // 16 * (32/R) column groups stride the columns (many loads in flight),
+    // partials summed in fixed group order
     const int2 tk = cta_tasks[blockIdx.x];
     const SnDev S = sn[tk.x];
-    const int r = tk.y + lane;
+    const int R = rows, ngrp = 32 / rows;
+    const int rl = lane % R, cg = lane / R;
+    const int r = tk.y + rl;
     const bool valid = r < S.nr;
-    const int cmax = (tk.y < S.nc) ? min(S.nc, tk.y + FW_ROWS) : S.nc;
+    const int cmax = (tk.y < S.nc) ? min(S.nc, tk.y + R) : S.nc;
     const double* Vs = V + 3 * (int64_t)S.rowoff;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     const double* Mp = M + S.valoff + (valid ? r : 0);
+    const int stride = FW_WARPS * ngrp;
     for (int c0 = 0; c0 < cmax; c0 += CH_FW) {
       const int c1 = min(cmax, c0 + CH_FW);
       __syncthreads();
       for (int q = threadIdx.x; q < 3 * (c1 - c0); q += blockDim.x) sm[q] = Vs[3 * c0 + q];
       __syncthreads();
       if (valid) {
-        int c = c0 + warp;
+        int c = c0 + warp * ngrp + cg;
 #pragma unroll 16
-        for (; c < c1; c += FW_WARPS) {
+        for (; c < c1; c += stride) {
           const double mv = Mp[(int64_t)c * S.nr];
           const double* v = sm + 3 * (c - c0);
           a0 += mv * v[0];
@@ -180,18 +201,18 @@ __global__ void __launch_bounds__(FW_THREADS) k_forward_level(const SnDev* __res
       }
     }
     __syncthreads();
-    double* red = sm;  // [FW_WARPS][32][3]
-    red[(warp * 32 + lane) * 3 + 0] = a0;
-    red[(warp * 32 + lane) * 3 + 1] = a1;
-    red[(warp * 32 + lane) * 3 + 2] = a2;
+    double* red = sm;  // [FW_WARPS * ngrp][R][3]
+    const int grp = warp * ngrp + cg;
+    red[(grp * R + rl) * 3 + 0] = a0;
+    red[(grp * R + rl) * 3 + 1] = a1;
+    red[(grp * R + rl) * 3 + 2] = a2;
     __syncthreads();
-    if (threadIdx.x < 96) {
-      const int rl = threadIdx.x / 3, q = threadIdx.x % 3;
-      const int rr = tk.y + rl;
+    if ((int)threadIdx.x < 3 * R) {
+      const int rr0 = threadIdx.x / 3, q = threadIdx.x % 3;
+      const int rr = tk.y + rr0;
       if (rr < S.nr) {
         double s = 0.0;
-#pragma unroll
-        for (int w = 0; w < FW_WARPS; ++w) s += red[(w * 32 + rl) * 3 + q];
+        for (int w = 0; w < stride; ++w) s += red[(w * R + rr0) * 3 + q];
         if (rr < S.nc) y[3 * (int64_t)(S.first + rr) + q] = s;
         else U[3 * (int64_t)(S.uoff + rr - S.nc) + q] = Vs[3 * rr + q] - s;
       }
@@ -550,6 +571,230 @@ __global__ void __launch_bounds__(SUB_THREADS) k_subtree_backward(
   }
 }
 
+// ------------------------------------------------------- dataflow sweeps
+// The upper levels (>= fuse) as ONE persistent launch per sweep: tasks are
+// claimed from a global counter in topological order (forward: leaves up;
+// backward: root down), and each waits only for the tasks it reads, through
+// per-supernode counters (release/acquire), instead of a kernel boundary per
+// level. Every claimed task waits only on earlier-claimed tasks, so a
+// persistent grid always makes progress. Summation orders are fixed (no float
+// atomics): bitwise-deterministic.
+constexpr int FL_FW_THREADS = 512;
+constexpr int FL_BW_THREADS = 256;
+constexpr int FL_ROWS = 32;
+
+__device__ __forceinline__ void flow_wait(const int* c, int need) {
+  if (threadIdx.x == 0 && need > 0) {
+    while (ld_relaxed(c) < need) {
+    }
+    fence_acq_rel_gpu();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int flow_claim(int* counter, int* slot) {
+  __syncthreads();  // the previous task is finished with the slot
+  if (threadIdx.x == 0) *slot = atomicAdd(counter, 1);
+  __syncthreads();
+  return *slot;
+}
+
+__global__ void __launch_bounds__(FL_FW_THREADS) k_forward_flow(
+    const SnDev* __restrict__ sn, const double* __restrict__ M, const int4* __restrict__ tasks, int ntasks,
+    const int* __restrict__ need, const int* __restrict__ parent, int* cnt /* [claim | done(ns) | gathered(ns)] */,
+    int ns, const int* __restrict__ owner, const int* __restrict__ ap, const int* __restrict__ as,
+    const double* __restrict__ b, double* V, double* y, double* U) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int slot;
+  int* done = cnt + 1;
+  int* gathered = cnt + 1 + ns;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    const int t = flow_claim(cnt, &slot);
+    if (t >= ntasks) break;
+    const int4 tk = tasks[t];
+    const SnDev S = sn[tk.y];
+    if (tk.x == 0) {
+      // gather: V = b (own columns) + children's update entries, fixed order
+      flow_wait(done + tk.y, need[tk.y]);
+      for (int k = threadIdx.x; k < S.nr; k += FL_FW_THREADS) {
+        const int p = S.rowoff + k;
+        const int o = owner[p];
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        if (o >= 0) {
+          v0 = b[3 * (int64_t)o + 0];
+          v1 = b[3 * (int64_t)o + 1];
+          v2 = b[3 * (int64_t)o + 2];
+        }
+        for (int q = ap[p]; q < ap[p + 1]; ++q) {
+          // written by other CTAs of this launch: bypass L1 (lines may be stale)
+          const double* u = U + 3 * (int64_t)as[q];
+          v0 += __ldcg(u + 0);
+          v1 += __ldcg(u + 1);
+          v2 += __ldcg(u + 2);
+        }
+        V[3 * (int64_t)p + 0] = v0;
+        V[3 * (int64_t)p + 1] = v1;
+        V[3 * (int64_t)p + 2] = v2;
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(gathered + tk.y, 1);
+      continue;
+    }
+    // rows r0..r0+31 of M_s (16 warps stride the columns), like k_forward_level
+    flow_wait(gathered + tk.y, 1);
+    const int r0 = tk.z;
+    const int r = r0 + lane;
+    const bool valid = r < S.nr;
+    const int cmax = (r0 < S.nc) ? min(S.nc, r0 + FL_ROWS) : S.nc;
+    const double* Vs = V + 3 * (int64_t)S.rowoff;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const double* Mp = M + S.valoff + (valid ? r : 0);
+    for (int c0 = 0; c0 < cmax; c0 += CH_FW) {
+      const int c1 = min(cmax, c0 + CH_FW);
+      __syncthreads();
+      for (int q = threadIdx.x; q < 3 * (c1 - c0); q += FL_FW_THREADS) sm[q] = __ldcg(Vs + 3 * c0 + q);
+      __syncthreads();
+      if (valid) {
+        int c = c0 + warp;
+#pragma unroll 16
+        for (; c < c1; c += FL_FW_THREADS / 32) {
+          const double mv = Mp[(int64_t)c * S.nr];
+          const double* v = sm + 3 * (c - c0);
+          a0 += mv * v[0];
+          a1 += mv * v[1];
+          a2 += mv * v[2];
+        }
+      }
+    }
+    __syncthreads();
+    double* red = sm;  // [16 warps][32][3]
+    red[(warp * 32 + lane) * 3 + 0] = a0;
+    red[(warp * 32 + lane) * 3 + 1] = a1;
+    red[(warp * 32 + lane) * 3 + 2] = a2;
+    __syncthreads();
+    if (threadIdx.x < 96) {
+      const int rl = threadIdx.x / 3, q = threadIdx.x % 3;
+      const int rr = r0 + rl;
+      if (rr < S.nr) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < FL_FW_THREADS / 32; ++w) s += red[(w * 32 + rl) * 3 + q];
+        if (rr < S.nc) y[3 * (int64_t)(S.first + rr) + q] = s;
+        else U[3 * (int64_t)(S.uoff + rr - S.nc) + q] = __ldcg(Vs + 3 * rr + q) - s;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && parent[tk.y] >= 0) atomicAdd(done + parent[tk.y], 1);
+  }
+}
+
+__global__ void __launch_bounds__(FL_BW_THREADS) k_backward_flow(
+    const SnDev* __restrict__ sn, const double* __restrict__ M, const int4* __restrict__ tasks,
+    const int* __restrict__ task_chunk, int ntasks, const int4* __restrict__ chunks, const int* __restrict__ need,
+    const int* __restrict__ parent, int* cnt /* [claim | done(ns) | gathered(ns) | chunk(nch)] */, int ns,
+    const int* __restrict__ owner, const int* __restrict__ rows, const double* __restrict__ y, double* Z, double* P,
+    double* XF) {
+  __shared__ double zs[3 * BT_ROWS];
+  __shared__ int slot, last;
+  int* done = cnt + 1;
+  int* gathered = cnt + 1 + ns;
+  int* chunk_cnt = cnt + 1 + 2 * ns;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    const int t = flow_claim(cnt, &slot);
+    if (t >= ntasks) break;
+    const int4 tk = tasks[t];
+    if (tk.x < 0) {
+      // gather z_s = [y own ; -x below]; the below rows are the ancestors' x
+      const int s = -tk.x - 1;
+      const SnDev S = sn[s];
+      if (parent[s] >= 0) flow_wait(done + parent[s], need[s]);
+      for (int k = threadIdx.x; k < S.nr; k += FL_BW_THREADS) {
+        const int p = S.rowoff + k;
+        const int o = owner[p];
+        double z0, z1, z2;
+        if (o >= 0) {
+          z0 = y[3 * (int64_t)o + 0];
+          z1 = y[3 * (int64_t)o + 1];
+          z2 = y[3 * (int64_t)o + 2];
+        } else {
+          const double* x = XF + 3 * (int64_t)rows[p];
+          z0 = -__ldcg(x + 0);
+          z1 = -__ldcg(x + 1);
+          z2 = -__ldcg(x + 2);
+        }
+        Z[3 * (int64_t)p + 0] = z0;
+        Z[3 * (int64_t)p + 1] = z1;
+        Z[3 * (int64_t)p + 2] = z2;
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release(gathered + s, 1);
+      continue;
+    }
+    // tile (s, c0, r0): partial x over rows [r0, r0+512) x columns [c0, c0+32)
+    const SnDev S = sn[tk.x];
+    flow_wait(gathered + tk.x, 1);
+    const int c0 = tk.y, r0 = tk.z;
+    const int nrt = min(BT_ROWS, S.nr - r0);
+    const double* Zs = Z + 3 * ((int64_t)S.rowoff + r0);
+    for (int q = threadIdx.x; q < 3 * nrt; q += FL_BW_THREADS) zs[q] = __ldcg(Zs + q);
+    __syncthreads();
+    double acc[4][3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.0;
+    const int cb = c0 + 4 * warp;
+    const double* Mt = M + S.valoff + (int64_t)cb * S.nr + r0;
+    const int nci = max(0, min(4, S.nc - cb));
+    if (nci > 0) {
+#pragma unroll 4
+      for (int k = lane; k < nrt; k += 32) {
+        const double z0 = zs[3 * k], z1 = zs[3 * k + 1], z2 = zs[3 * k + 2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < nci) {
+            const double m = Mt[(int64_t)i * S.nr + k];
+            acc[i][0] += m * z0;
+            acc[i][1] += m * z1;
+            acc[i][2] += m * z2;
+          }
+        }
+      }
+    }
+    double* out = P + (int64_t)tk.w * (BT_COLS * 3);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double v = warp_sum(acc[i][q]);
+        if (lane == 0) out[(4 * warp + i) * 3 + q] = v;
+      }
+    // the last tile of the column chunk sums the partials in row-tile order
+    __threadfence();
+    __syncthreads();
+    const int ch = task_chunk[t];
+    const int4 C = chunks[ch];
+    if (threadIdx.x == 0) last = (atomicAdd(chunk_cnt + ch, 1) == C.w - 1);
+    __syncthreads();
+    if (!last) continue;
+    __threadfence();
+    if (threadIdx.x < BT_COLS * 3) {
+      const int cc = threadIdx.x / 3, q = threadIdx.x % 3;
+      if (C.y + cc < S.nc) {
+        double s = 0.0;
+        for (int k = 0; k < C.w; ++k) s += __ldcg(P + ((int64_t)(C.z + k) * BT_COLS + cc) * 3 + q);
+        XF[3 * (int64_t)(S.first + C.y + cc) + q] = s;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(done + tk.x, 1);
+  }
+}
+
 // ---------------------------------------------------------------- host
 template <typename T>
 static int upload(T** dst, const std::vector<T>& v) {
@@ -652,14 +897,25 @@ int build_device_factor(Factor& f) {
     d->bwt_off[l] = (int)bwt.size();
     d->bwr_off[l] = (int)bwr.size();
     d->bww_off[l] = (int)bww.size();
+    {
+      // forward CTA task height: the largest of 32/16/8 rows giving >= 4 waves
+      int64_t n32 = 0;
+      for (int64_t s : bylevel[l])
+        if (sn[s].nc > WARP_NC) n32 += (sn[s].nr + 31) / 32;
+      static const int waves = getenv("SPB_FW_WAVES") ? std::max(1, atoi(getenv("SPB_FW_WAVES"))) : 2;
+      T.rows = n32 >= waves * NUM_SMS_B200 ? 32 : (2 * n32 >= waves * NUM_SMS_B200 ? 16 : 8);
+      for (int64_t s : bylevel[l]) {
+        const SnDev& S = sn[s];
+        if (S.nc <= WARP_NC) continue;
+        for (int r0 = 0; r0 < S.nr; r0 += T.rows) fwc.push_back(make_int2((int)s, r0));
+        T.max_nc = std::max(T.max_nc, S.nc);
+      }
+    }
     for (int64_t s : bylevel[l]) {
       const SnDev& S = sn[s];
       const bool small = S.nc <= WARP_NC;
       if (small) {
         for (int r0 = 0; r0 < S.nr; r0 += FW_WROWS) fww.push_back(make_int2((int)s, r0));
-      } else {
-        for (int r0 = 0; r0 < S.nr; r0 += FW_ROWS) fwc.push_back(make_int2((int)s, r0));
-        T.max_nc = std::max(T.max_nc, S.nc);
       }
       if (small && S.nr <= BW_WARP_MAXNR) {
         bww.push_back((int)s);
@@ -683,7 +939,7 @@ int build_device_factor(Factor& f) {
   d->bwr_off[f.nlevels] = (int)bwr.size();
   d->bww_off[f.nlevels] = (int)bww.size();
   // ---- bottom subtrees: choose the fuse height f by a small cost model
-  // (slowest group's panel bytes at ~15 GB/s effective per SM + ~20 us per remaining
+  // (slowest group's panel bytes at ~25 GB/s effective per SM + ~20 us per remaining
   // level launch pair), group whole subtrees (LPT on bytes, 148 groups)
   {
     std::vector<std::vector<int64_t>> kids(ns);
@@ -719,7 +975,7 @@ int build_device_factor(Factor& f) {
         group_of_root[k] = gmin;
       }
       const double maxb = 8.0 * *std::max_element(load.begin(), load.end());
-      return maxb / 15e9 + 20e-6 * (double)(f.nlevels - fz);
+      return maxb / 25e9 + 20e-6 * (double)(f.nlevels - fz);
     };
     int best = 0;
     double best_t = 20e-6 * (double)f.nlevels;
@@ -771,6 +1027,60 @@ int build_device_factor(Factor& f) {
       return rc2;
     }
   }
+  // ---- dataflow task lists for the levels >= fuse
+  size_t flow_slots = 0;
+  {
+    const char* fe = getenv("SPB_SWEEP_FLOW");
+    // experimental (SPB_SWEEP_FLOW=1): on cfg3 the per-level launches are
+    // faster, since a persistent CTA serialises its tasks' latency chains
+    d->flow = fe ? atoi(fe) : 0;
+    std::vector<int> par(ns), fneed(ns, 0), bneed(ns, 0), bchunk_of;
+    std::vector<int4> ft, bt, bch;
+    std::vector<int> nch_of(ns, 0);
+    for (int64_t s = 0; s < ns; ++s) par[s] = (int)f.sn_parent[s];
+    for (int64_t l = d->fuse; l < f.nlevels; ++l)
+      for (int64_t s : bylevel[l]) {
+        ft.push_back(make_int4(0, (int)s, 0, 0));
+        for (int r0 = 0; r0 < sn[s].nr; r0 += FL_ROWS) ft.push_back(make_int4(1, (int)s, r0, 0));
+        if (par[s] >= 0) fneed[par[s]] += (sn[s].nr + FL_ROWS - 1) / FL_ROWS;
+      }
+    int slot = 0;
+    for (int64_t l = f.nlevels - 1; l >= d->fuse; --l)
+      for (int64_t s : bylevel[l]) {
+        bt.push_back(make_int4(-(int)(s + 1), 0, 0, 0));
+        bchunk_of.push_back(-1);
+        const SnDev& S = sn[s];
+        for (int c0 = 0; c0 < S.nc; c0 += BT_COLS) {
+          const int slot0 = slot, ch = (int)bch.size();
+          for (int r0 = 0; r0 < S.nr; r0 += BT_ROWS) {
+            if (r0 + BT_ROWS <= c0) continue;  // entirely above the diagonal of inv(L_ss): zero
+            bt.push_back(make_int4((int)s, c0, r0, slot++));
+            bchunk_of.push_back(ch);
+          }
+          bch.push_back(make_int4((int)s, c0, slot0, slot - slot0));
+          nch_of[s]++;
+        }
+      }
+    for (int64_t s = 0; s < ns; ++s)
+      if (f.sn_level[s] >= d->fuse && par[s] >= 0) bneed[s] = nch_of[par[s]];
+    int maxnc = 0;
+    for (int64_t s = 0; s < ns; ++s)
+      if (f.sn_level[s] >= d->fuse) maxnc = std::max(maxnc, sn[s].nc);
+    d->fw_smem = sizeof(double) * std::max(3 * std::min(maxnc, CH_FW), 3 * FL_FW_THREADS);
+    d->nft = (int)ft.size();
+    d->nbt = (int)bt.size();
+    d->nbch = (int)bch.size();
+    flow_slots = (size_t)slot;
+    std::vector<int> zero(1 + 2 * ns + bch.size(), 0);
+    int rc3;
+    if ((rc3 = upload(&d->parent, par)) || (rc3 = upload(&d->ftasks, ft)) || (rc3 = upload(&d->f_need, fneed)) ||
+        (rc3 = upload(&d->btasks, bt)) || (rc3 = upload(&d->btask_chunk, bchunk_of)) ||
+        (rc3 = upload(&d->bchunks, bch)) || (rc3 = upload(&d->b_need, bneed)) ||
+        (rc3 = upload(&d->flow_cnt, zero))) {
+      delete d;
+      return rc3;
+    }
+  }
   int rc;
   if ((rc = upload(&d->sn, sn)) || (rc = upload(&d->rows, rows)) || (rc = upload(&d->pos_owner, owner)) ||
       (rc = upload(&d->lvl_pos, lpos)) || (rc = upload(&d->M, f.Mval)) || (rc = upload(&d->asm_ptr, cnt)) ||
@@ -782,7 +1092,8 @@ int build_device_factor(Factor& f) {
     return rc;
   }
   if (cudaMalloc(&d->VZ, sizeof(double) * 3 * std::max<int64_t>(d->nrows_total, 1)) != cudaSuccess ||
-      cudaMalloc(&d->P, sizeof(double) * 3 * BT_COLS * std::max<size_t>(bwt.size(), 1)) != cudaSuccess) {
+      cudaMalloc(&d->P, sizeof(double) * 3 * BT_COLS * std::max<size_t>(std::max(bwt.size(), flow_slots), 1)) !=
+          cudaSuccess) {
     delete d;
     set_error("cudaMalloc failed (sweep buffer)");
     return SPB_ERR_CUDA;
@@ -790,7 +1101,16 @@ int build_device_factor(Factor& f) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_forward_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
+    cudaFuncSetAttribute(k_forward_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
     attr = true;
+  }
+  // persistent grids: exactly the resident CTAs
+  {
+    int nf = 0, nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nf, k_forward_flow, FL_FW_THREADS, d->fw_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_backward_flow, FL_BW_THREADS, 0);
+    d->fw_grid = std::max(1, nf) * NUM_SMS_B200;
+    d->bw_grid = std::max(1, nb) * NUM_SMS_B200;
   }
   f.dev = d;
   return SPB_OK;
@@ -804,7 +1124,14 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
                                                          d.VZ, y, U);
     if (launches) ++*launches;
   }
-  for (int l = d.fuse; l < d.nlevels; ++l) {
+  if (d.flow && d.nft > 0) {
+    cudaMemsetAsync(d.flow_cnt, 0, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch), st);
+    k_forward_flow<<<d.fw_grid, FL_FW_THREADS, d.fw_smem, st>>>(d.sn, d.M, d.ftasks, d.nft, d.f_need, d.parent,
+                                                                  d.flow_cnt, d.ns, d.pos_owner, d.asm_ptr, d.asm_src,
+                                                                  b, d.VZ, y, U);
+    if (launches) ++*launches;
+  }
+  for (int l = d.fuse; l < d.nlevels && !d.flow; ++l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
     k_fw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.asm_ptr,
@@ -813,7 +1140,7 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
     const size_t smem =
         T.ncta ? std::max<size_t>(sizeof(double) * 3 * std::min(T.max_nc, CH_FW), FW_WARPS * 32 * 3 * 8) : 0;
     k_forward_level<<<grid, FW_THREADS, smem, st>>>(d.sn, d.M, d.VZ, d.fw_cta + T.cta_off, T.ncta, d.fw_warp + T.warp_off,
-                                             T.nwarp, y, U);
+                                             T.nwarp, T.rows, y, U);
     if (launches) *launches += 2;
   }
   if (d.n2 > 0) {
@@ -823,7 +1150,14 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
 }
 
 void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches) {
-  for (int l = d.nlevels - 1; l >= d.fuse; --l) {
+  if (d.flow && d.nbt > 0) {
+    cudaMemsetAsync(d.flow_cnt, 0, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch), st);
+    k_backward_flow<<<d.bw_grid, FL_BW_THREADS, 0, st>>>(d.sn, d.M, d.btasks, d.btask_chunk, d.nbt, d.bchunks,
+                                                                d.b_need, d.parent, d.flow_cnt, d.ns, d.pos_owner,
+                                                                d.rows, y, d.VZ, d.P, XF);
+    if (launches) ++*launches;
+  }
+  for (int l = d.nlevels - 1; l >= d.fuse && !d.flow; --l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
     k_bw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.rows, y, XF,

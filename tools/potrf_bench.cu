@@ -1,5 +1,6 @@
 // Microbenchmark of the diagonal-tile factorization pieces (diagnostics).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2008_01541_b200/csrc potrf_bench.cu ...
+#define SPB_POTRF_PROF 1
 #include "../paper_2008_01541_b200/csrc/dense.cu"
 
 namespace spb {
@@ -60,6 +61,18 @@ int main() {
   cudaMemcpy(&hi, info, 4, cudaMemcpyDeviceToHost);
   printf("err=%s info=%d potrf_blocked %lld cyc (%.2f us @1.9GHz), diag16 %lld cyc, cons_sync %lld cyc\n",
          cudaGetErrorString(cudaGetLastError()), hi, h[0], h[0] / 1900.0, h[1], h[2]);
+  long long prof[32];
+  cudaMemcpyFromSymbol(prof, g_potrf_prof, sizeof(prof));
+  // phases are cumulative clocks over 20 reps (+ the diag16-only loop does not mark)
+  const char* names[15] = {"start", "init", "upd+d16_0", "pan_0", "upd+d16_1", "pan_1", "upd+d16_2", "pan_2",
+                           "upd+d16_3", "pan_3", "", "", "", "", "store"};
+  long long prev = prof[1];
+  printf("  %-10s %8.0f cyc\n", "init", (prof[1] - prof[0]) / 20.0);
+  for (int k = 2; k < 10; ++k) {
+    printf("  %-10s %8.0f cyc\n", names[k], (prof[k] - prev) / 20.0);
+    prev = prof[k];
+  }
+  printf("  %-10s %8.0f cyc\n", "store", (prof[14] - prev) / 20.0);
   double hL[4096];
   cudaMemcpy(hL, L, 4096 * 8, cudaMemcpyDeviceToHost);
   // check L L^T == A
