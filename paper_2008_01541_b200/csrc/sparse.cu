@@ -37,7 +37,8 @@ struct LevelTasks {
   int cta_off, ncta, warp_off, nwarp;
   int pos_off, npos;  // struct positions of the level (gather kernels)
   int max_nc;         // forward CTA tasks: columns staged in smem
-  int rows;           // forward CTA task height (32, 16 or 8: >= ~4 waves per level)
+  int rows;           // forward CTA task height (8..128)
+  int bw_rows;        // backward tile height (128..4096)
 };
 
 struct DeviceFactor {
@@ -57,6 +58,8 @@ struct DeviceFactor {
   int2* fw_warp = nullptr;  // (s, row0)
   int4* bw_tiles = nullptr;   // (s, c0, r0, partial slot)
   int4* bw_chunks = nullptr;  // (s, c0, first slot, ntiles)
+  int* bw_tile_chunk = nullptr;  // chunk (global index) of every tile
+  int* bw_chunk_cnt = nullptr;   // arrivals per chunk, zeroed per sweep
   double* P = nullptr;        // backward tile partials
   int* bw_warp = nullptr;     // s
   // bottom subtrees (levels < fuse): one CTA per group walks its supernodes
@@ -87,7 +90,7 @@ struct DeviceFactor {
                     (void*)asm_ptr, (void*)asm_src, (void*)x2_ptr, (void*)x2_src, (void*)fw_cta, (void*)fw_warp,
                     (void*)bw_tiles, (void*)bw_chunks, (void*)P, (void*)bw_warp, (void*)sub_pos,
                     (void*)sub_pos_off, (void*)sub_fw, (void*)sub_fw_off, (void*)sub_bw, (void*)sub_bw_off,
-                    (void*)parent, (void*)ftasks, (void*)f_need, (void*)btasks, (void*)btask_chunk,
+                    (void*)bw_tile_chunk, (void*)bw_chunk_cnt, (void*)parent, (void*)ftasks, (void*)f_need, (void*)btasks, (void*)btask_chunk,
                     (void*)bchunks, (void*)b_need, (void*)flow_cnt})
       if (p) cudaFree(p);
   }
@@ -112,17 +115,20 @@ constexpr int CH_FW = 4096;     // forward column chunk staged in smem
 __global__ void k_fw_gather(const int* __restrict__ lvl_pos, int npos, const int* __restrict__ owner,
                             const int* __restrict__ ap, const int* __restrict__ as, const double* __restrict__ U,
                             const double* __restrict__ b, double* __restrict__ V) {
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= npos) return;
   const int p = lvl_pos[t];
   const int o = owner[p];
+  const int k0 = ap[p], k1 = ap[p + 1];
+  pdl_wait();  // U from the previous level
   double v0 = 0.0, v1 = 0.0, v2 = 0.0;
   if (o >= 0) {
     v0 = b[3 * (int64_t)o + 0];
     v1 = b[3 * (int64_t)o + 1];
     v2 = b[3 * (int64_t)o + 2];
   }
-  for (int k = ap[p]; k < ap[p + 1]; ++k) {
+  for (int k = k0; k < k1; ++k) {
     const double* u = U + 3 * (int64_t)as[k];
     v0 += u[0];
     v1 += u[1];
@@ -260,9 +266,11 @@ __global__ void __launch_bounds__(FW_THREADS) k_forward_level(const SnDev* __res
 // f~2[k] = f2[k] + sum of root update entries on x2 row k (= f2 - C y1).
 __global__ void k_forward_x2(int n1, int n2, const int* __restrict__ xp, const int* __restrict__ xs,
                              const double* __restrict__ U, const double* __restrict__ b, double* __restrict__ f2) {
+  pdl_trigger();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= 3 * n2) return;
   int row = k / 3, q = k % 3;
+  pdl_wait();
   double v = b[3 * (int64_t)(n1 + row) + q];
   for (int t = xp[row]; t < xp[row + 1]; ++t) v += U[3 * (int64_t)xs[t] + q];
   f2[k] = v;
@@ -383,6 +391,220 @@ __global__ void __launch_bounds__(256) k_backward_warp(const SnDev* __restrict__
   }
 }
 
+// --------------------------------------------- fused level kernels (>= fuse)
+// One launch per level and sweep: the gathers are folded into the GEMV tasks
+// (each task assembles the inputs it reads) and the backward column-chunk
+// reduction is done by the chunk's last tile (atomic arrival count; the sum
+// itself runs in fixed row-tile order), so a level costs one launch instead of
+// 2 (forward) or 3-4 (backward).
+__device__ __forceinline__ double bw_gather_q(int p, int q, const int* __restrict__ owner,
+                                              const int* __restrict__ rows, const double* __restrict__ y,
+                                              const double* __restrict__ XF) {
+  const int o = owner[p];
+  return o >= 0 ? y[3 * (int64_t)o + q] : -XF[3 * (int64_t)rows[p] + q];
+}
+
+// CTA task (s, r0): rows r0 .. r0 + R - 1, R in {8, ..., 128}: lanes cover
+// RL = min(R, 32) rows x 32/RL column subgroups, warps cover G = R/32 row
+// groups x 16/G column groups; every thread strides its column group.
+__global__ void __launch_bounds__(FW_THREADS) k_fw_level(
+    const SnDev* __restrict__ sn, const double* __restrict__ M, const int2* __restrict__ cta_tasks, int ncta,
+    const int2* __restrict__ warp_tasks, int nwarp, int R, const double* __restrict__ V, double* __restrict__ y,
+    double* __restrict__ U) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_trigger();
+  if ((int)blockIdx.x < ncta) {
+    const int2 tk = cta_tasks[blockIdx.x];
+    const SnDev S = sn[tk.x];
+    const double* Vs = V + 3 * (int64_t)S.rowoff;
+    pdl_wait();  // V comes from this level's gather
+    const int r0 = tk.y;
+    const int RL = min(R, 32), G = max(1, R >> 5);
+    const int rg = warp % G, row_in = 32 * rg + lane % RL;
+    const int cgi = (warp / G) * (32 / RL) + lane / RL, ncg = (FW_WARPS / G) * (32 / RL);
+    const int r = r0 + row_in;
+    const bool valid = r < S.nr && row_in < R;
+    const int cmax = (r0 < S.nc) ? min(S.nc, r0 + R) : S.nc;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const double* Mp = M + S.valoff + (valid ? r : 0);
+    for (int c0 = 0; c0 < cmax; c0 += CH_FW) {
+      const int c1 = min(cmax, c0 + CH_FW);
+      __syncthreads();
+      for (int e = threadIdx.x; e < 3 * (c1 - c0); e += FW_THREADS) sm[e] = Vs[3 * c0 + e];
+      __syncthreads();
+      if (valid) {
+        int c = c0 + cgi;
+#pragma unroll 16
+        for (; c < c1; c += ncg) {
+          const double mv = Mp[(int64_t)c * S.nr];
+          const double* v = sm + 3 * (c - c0);
+          a0 += mv * v[0];
+          a1 += mv * v[1];
+          a2 += mv * v[2];
+        }
+      }
+    }
+    __syncthreads();
+    double* red = sm;  // [column group][row in task][3]
+    if (row_in < R) {
+      const int e0 = (cgi * R + row_in) * 3;
+      red[e0 + 0] = a0;
+      red[e0 + 1] = a1;
+      red[e0 + 2] = a2;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 3 * R; e += FW_THREADS) {
+      const int rl = e / 3, q = e % 3;
+      const int rr = r0 + rl;
+      if (rr >= S.nr) continue;
+      double sum = 0.0;
+      for (int g2 = 0; g2 < ncg; ++g2) sum += red[(g2 * R + rl) * 3 + q];
+      if (rr < S.nc) y[3 * (int64_t)(S.first + rr) + q] = sum;
+      else U[3 * (int64_t)(S.uoff + rr - S.nc) + q] = Vs[3 * rr + q] - sum;
+    }
+  } else {
+    const int t = ((int)blockIdx.x - ncta) * FW_WARPS + warp;
+    if (t >= nwarp) return;
+    const int2 tk = warp_tasks[t];
+    const SnDev S = sn[tk.x];
+    const double* Vs = V + 3 * (int64_t)S.rowoff;
+    pdl_wait();
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    if (lane < S.nc) {
+      v0 = Vs[3 * lane + 0];
+      v1 = Vs[3 * lane + 1];
+      v2 = Vs[3 * lane + 2];
+    }
+    const int r = tk.y + lane;
+    const bool valid = r < S.nr;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const double* Mp = M + S.valoff + (valid ? r : 0);
+#pragma unroll
+    for (int c = 0; c < WARP_NC; ++c) {
+      if (c < S.nc) {
+        const double mv = valid ? Mp[(int64_t)c * S.nr] : 0.0;
+        a0 += mv * __shfl_sync(0xffffffffu, v0, c);
+        a1 += mv * __shfl_sync(0xffffffffu, v1, c);
+        a2 += mv * __shfl_sync(0xffffffffu, v2, c);
+      }
+    }
+    if (valid) {
+      if (r < S.nc) {
+        y[3 * (int64_t)(S.first + r) + 0] = a0;
+        y[3 * (int64_t)(S.first + r) + 1] = a1;
+        y[3 * (int64_t)(S.first + r) + 2] = a2;
+      } else {
+        const int64_t o = 3 * (int64_t)(S.uoff + r - S.nc);
+        U[o + 0] = Vs[3 * r + 0] - a0;
+        U[o + 1] = Vs[3 * r + 1] - a1;
+        U[o + 2] = Vs[3 * r + 2] - a2;
+      }
+    }
+  }
+}
+
+// Tile (s, c0, r0): rows [r0, r0 + RT) x columns [c0, c0 + 32) of M_s (RT per
+// level, sized so the level's tiles fit the resident CTA slots); z gathered
+// straight into shared memory.
+__global__ void __launch_bounds__(256) k_bw_level(
+    const SnDev* __restrict__ sn, const double* __restrict__ M, const int4* __restrict__ tiles, int RT,
+    const int* __restrict__ tile_chunk, const int4* __restrict__ chunks, int* __restrict__ chunk_cnt,
+    const int* __restrict__ owner, const int* __restrict__ rows, const double* __restrict__ y,
+    double* __restrict__ P, double* __restrict__ XF) {
+  extern __shared__ double zs[];  // 3 x RT
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_trigger();
+  const int4 tk = tiles[blockIdx.x];  // (s, c0, r0, slot)
+  const SnDev S = sn[tk.x];
+  const int c0 = tk.y, r0 = tk.z;
+  const int nrt = min(RT, S.nr - r0);
+  pdl_wait();  // x of the ancestors (previous level) and the chunk counters
+  for (int e = threadIdx.x; e < 3 * nrt; e += 256) zs[e] = bw_gather_q(S.rowoff + r0 + e / 3, e % 3, owner, rows, y, XF);
+  __syncthreads();
+  double acc[4][3];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.0;
+  const int cb = c0 + 4 * warp;
+  const double* Mt = M + S.valoff + (int64_t)cb * S.nr + r0;
+  const int nci = max(0, min(4, S.nc - cb));
+  if (nci > 0) {
+#pragma unroll 4
+    for (int k = lane; k < nrt; k += 32) {
+      const double z0 = zs[3 * k], z1 = zs[3 * k + 1], z2 = zs[3 * k + 2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < nci) {
+          const double m = Mt[(int64_t)i * S.nr + k];
+          acc[i][0] += m * z0;
+          acc[i][1] += m * z1;
+          acc[i][2] += m * z2;
+        }
+      }
+    }
+  }
+  double* out = P + (int64_t)tk.w * (BT_COLS * 3);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const double v = warp_sum(acc[i][q]);
+      if (lane == 0) out[(4 * warp + i) * 3 + q] = v;
+    }
+  // the chunk's last tile sums the partials in row-tile order
+  __threadfence();
+  __syncthreads();
+  const int ch = tile_chunk[blockIdx.x];
+  const int4 C = chunks[ch];  // (s, c0, first slot, ntiles)
+  if (threadIdx.x == 0) last = (atomicAdd(chunk_cnt + ch, 1) == C.w - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < BT_COLS * 3) {
+    const int cc = threadIdx.x / 3, q = threadIdx.x % 3;
+    if (C.y + cc < S.nc) {
+      double sum = 0.0;
+      for (int k = 0; k < C.w; ++k) sum += __ldcg(P + ((int64_t)(C.z + k) * BT_COLS + cc) * 3 + q);
+      XF[3 * (int64_t)(S.first + C.y + cc) + q] = sum;
+    }
+  }
+}
+
+// warp task (s), nc <= 16 and nr <= BW_WARP_MAXNR: lanes over rows, one RHS at
+// a time, butterfly (separate kernel: rare above the fused subtrees)
+__global__ void __launch_bounds__(256) k_bw_level_warp(const SnDev* __restrict__ sn, const double* __restrict__ M,
+                                                       const int* __restrict__ warp_tasks, int nwarp,
+                                                       const int* __restrict__ owner, const int* __restrict__ rows,
+                                                       const double* __restrict__ y, double* __restrict__ XF) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_trigger();
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= nwarp) return;
+  const SnDev S = sn[warp_tasks[t]];
+  const double* Mc = M + S.valoff;
+  pdl_wait();
+  double out[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    double acc[16];
+#pragma unroll
+    for (int cc = 0; cc < 16; ++cc) acc[cc] = 0.0;
+    for (int r = lane; r < S.nr; r += 32) {
+      const double z = bw_gather_q(S.rowoff + r, q, owner, rows, y, XF);
+#pragma unroll
+      for (int cc = 0; cc < 16; ++cc)
+        if (cc < S.nc) acc[cc] += Mc[(int64_t)cc * S.nr + r] * z;
+    }
+    out[q] = warp_transpose_sum16(acc, lane);
+  }
+  if (lane < S.nc) {
+    XF[3 * (int64_t)(S.first + lane) + 0] = out[0];
+    XF[3 * (int64_t)(S.first + lane) + 1] = out[1];
+    XF[3 * (int64_t)(S.first + lane) + 2] = out[2];
+  }
+}
+
 // ------------------------------------------------- bottom-subtree kernels
 // The lower elimination-tree levels hold thousands of small supernodes
 // (cfg3: levels 0-6 = 5.5K supernodes, 105 MB of panels) whose per-level
@@ -466,6 +688,8 @@ __global__ void __launch_bounds__(SUB_THREADS) k_subtree_forward(
     const int* __restrict__ owner, const int* __restrict__ ap, const int* __restrict__ as,
     const double* __restrict__ b, double* V, double* y, double* U) {
   const int g = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_trigger();
+  pdl_wait();
   for (int l = 0; l < fuse; ++l) {
     const int q0 = pos_off[g * fuse + l], q1 = pos_off[g * fuse + l + 1];
     for (int t = q0 + (int)threadIdx.x; t < q1; t += SUB_THREADS) {
@@ -503,6 +727,8 @@ __global__ void __launch_bounds__(SUB_THREADS) k_subtree_backward(
     const int* __restrict__ owner, const int* __restrict__ rows, const double* __restrict__ y, double* Z,
     double* XF) {
   const int g = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_trigger();
+  pdl_wait();
   for (int l = fuse - 1; l >= 0; --l) {
     const int q0 = pos_off[g * fuse + l], q1 = pos_off[g * fuse + l + 1];
     for (int t = q0 + (int)threadIdx.x; t < q1; t += SUB_THREADS) {
@@ -882,6 +1108,7 @@ int build_device_factor(Factor& f) {
   for (int64_t s = 0; s < ns; ++s) bylevel[f.sn_level[s]].push_back(s);
   std::vector<int2> fwc, fww;
   std::vector<int4> bwt, bwr;
+  std::vector<int> btc;
   std::vector<int> bww, lpos;
   lpos.reserve(d->nrows_total);
   d->lv.resize(f.nlevels);
@@ -902,13 +1129,48 @@ int build_device_factor(Factor& f) {
       int64_t n32 = 0;
       for (int64_t s : bylevel[l])
         if (sn[s].nc > WARP_NC) n32 += (sn[s].nr + 31) / 32;
-      static const int waves = getenv("SPB_FW_WAVES") ? std::max(1, atoi(getenv("SPB_FW_WAVES"))) : 2;
-      T.rows = n32 >= waves * NUM_SMS_B200 ? 32 : (2 * n32 >= waves * NUM_SMS_B200 ? 16 : 8);
+      // task height R: the smallest of 8..128 whose task count still fits
+      // the resident CTA slots (~4 x 148): a task streams at a roughly fixed
+      // rate, so the level is fastest when all of it runs concurrently in as
+      // many tasks as possible (wide top levels: short tasks; levels of many
+      // small supernodes: tall tasks, one wave)
+      static const int slots = (getenv("SPB_FW_SLOTS") ? atoi(getenv("SPB_FW_SLOTS")) : 4) * NUM_SMS_B200;
+      (void)n32;
+      T.rows = 128;
+      for (int R = 8; R <= 128; R *= 2) {
+        int64_t nt = 0;
+        for (int64_t s : bylevel[l])
+          if (sn[s].nc > WARP_NC) nt += (sn[s].nr + R - 1) / R;
+        if (nt <= slots) {
+          T.rows = R;
+          break;
+        }
+      }
       for (int64_t s : bylevel[l]) {
         const SnDev& S = sn[s];
         if (S.nc <= WARP_NC) continue;
         for (int r0 = 0; r0 < S.nr; r0 += T.rows) fwc.push_back(make_int2((int)s, r0));
         T.max_nc = std::max(T.max_nc, S.nc);
+      }
+    }
+    {
+      // backward tile height: the smallest of 128..4096 whose tile count fits
+      // the resident slots (~4 x 148 CTAs of 256 threads; swept on cfg3)
+      static const int bslots = (getenv("SPB_BW_SLOTS") ? atoi(getenv("SPB_BW_SLOTS")) : 4) * NUM_SMS_B200;
+      T.bw_rows = 4096;
+      for (int RT = 128; RT <= 4096; RT *= 2) {
+        int64_t nt = 0;
+        for (int64_t s : bylevel[l]) {
+          const SnDev& S = sn[s];
+          if (S.nc <= WARP_NC && S.nr <= BW_WARP_MAXNR) continue;
+          for (int c0 = 0; c0 < S.nc; c0 += BT_COLS)
+            for (int r0 = 0; r0 < S.nr; r0 += RT)
+              if (r0 + RT > c0) ++nt;
+        }
+        if (nt <= bslots) {
+          T.bw_rows = RT;
+          break;
+        }
       }
     }
     for (int64_t s : bylevel[l]) {
@@ -920,12 +1182,14 @@ int build_device_factor(Factor& f) {
       if (small && S.nr <= BW_WARP_MAXNR) {
         bww.push_back((int)s);
       } else {
+        const int RT = l < d->fuse ? BT_ROWS : T.bw_rows;
         for (int c0 = 0; c0 < S.nc; c0 += BT_COLS) {
           const int slot0 = (int)bwt.size();
-          for (int r0 = 0; r0 < S.nr; r0 += BT_ROWS) {
-            if (r0 + BT_ROWS <= c0) continue;  // entirely above the diagonal of inv(L_ss): zero
+          for (int r0 = 0; r0 < S.nr; r0 += RT) {
+            if (r0 + RT <= c0) continue;  // entirely above the diagonal of inv(L_ss): zero
             bwt.push_back(make_int4((int)s, c0, r0, (int)bwt.size()));
           }
+          for (int k = slot0; k < (int)bwt.size(); ++k) btc.push_back((int)bwr.size());
           bwr.push_back(make_int4((int)s, c0, slot0, (int)bwt.size() - slot0));
         }
       }
@@ -1086,7 +1350,8 @@ int build_device_factor(Factor& f) {
       (rc = upload(&d->lvl_pos, lpos)) || (rc = upload(&d->M, f.Mval)) || (rc = upload(&d->asm_ptr, cnt)) ||
       (rc = upload(&d->asm_src, asrc)) || (rc = upload(&d->x2_ptr, xcnt)) || (rc = upload(&d->x2_src, xsrc)) ||
       (rc = upload(&d->fw_cta, fwc)) || (rc = upload(&d->fw_warp, fww)) || (rc = upload(&d->bw_tiles, bwt)) ||
-      (rc = upload(&d->bw_chunks, bwr)) ||
+      (rc = upload(&d->bw_chunks, bwr)) || (rc = upload(&d->bw_tile_chunk, btc)) ||
+      (rc = upload(&d->bw_chunk_cnt, std::vector<int>(std::max<size_t>(bwr.size(), 1), 0))) ||
       (rc = upload(&d->bw_warp, bww))) {
     delete d;
     return rc;
@@ -1102,6 +1367,8 @@ int build_device_factor(Factor& f) {
   if (!attr) {
     cudaFuncSetAttribute(k_forward_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
     cudaFuncSetAttribute(k_forward_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
+    cudaFuncSetAttribute(k_fw_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
+    cudaFuncSetAttribute(k_bw_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 8);
     attr = true;
   }
   // persistent grids: exactly the resident CTAs
@@ -1119,9 +1386,9 @@ int build_device_factor(Factor& f) {
 void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
                     int* launches) {
   if (d.fuse > 0) {
-    k_subtree_forward<<<d.ngroups, SUB_THREADS, 0, st>>>(d.sn, d.M, d.sub_pos, d.sub_pos_off, d.sub_fw,
-                                                         d.sub_fw_off, d.fuse, d.pos_owner, d.asm_ptr, d.asm_src, b,
-                                                         d.VZ, y, U);
+    launch_pdl(k_subtree_forward, dim3(d.ngroups), dim3(SUB_THREADS), 0, st, (const SnDev*)d.sn, (const double*)d.M,
+               (const int*)d.sub_pos, (const int*)d.sub_pos_off, (const int2*)d.sub_fw, (const int*)d.sub_fw_off,
+               d.fuse, (const int*)d.pos_owner, (const int*)d.asm_ptr, (const int*)d.asm_src, b, d.VZ, y, U);
     if (launches) ++*launches;
   }
   if (d.flow && d.nft > 0) {
@@ -1134,17 +1401,19 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
   for (int l = d.fuse; l < d.nlevels && !d.flow; ++l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
-    k_fw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.asm_ptr,
-                                                       d.asm_src, U, b, d.VZ);
+    launch_pdl(k_fw_gather, dim3(ceil_div(T.npos, 256)), dim3(256), 0, st, (const int*)(d.lvl_pos + T.pos_off),
+               T.npos, (const int*)d.pos_owner, (const int*)d.asm_ptr, (const int*)d.asm_src, (const double*)U, b,
+               d.VZ);
     const int grid = T.ncta + (T.nwarp + FW_WARPS - 1) / FW_WARPS;
-    const size_t smem =
-        T.ncta ? std::max<size_t>(sizeof(double) * 3 * std::min(T.max_nc, CH_FW), FW_WARPS * 32 * 3 * 8) : 0;
-    k_forward_level<<<grid, FW_THREADS, smem, st>>>(d.sn, d.M, d.VZ, d.fw_cta + T.cta_off, T.ncta, d.fw_warp + T.warp_off,
-                                             T.nwarp, T.rows, y, U);
+    const size_t smem = sizeof(double) * std::max(3 * std::min(T.max_nc, CH_FW), 3 * FW_THREADS);
+    launch_pdl(k_fw_level, dim3(grid), dim3(FW_THREADS), smem, st, (const SnDev*)d.sn, (const double*)d.M,
+               (const int2*)(d.fw_cta + T.cta_off), T.ncta, (const int2*)(d.fw_warp + T.warp_off), T.nwarp,
+               T.rows, (const double*)d.VZ, y, U);
     if (launches) *launches += 2;
   }
   if (d.n2 > 0) {
-    k_forward_x2<<<ceil_div(3 * (int64_t)d.n2, 256), 256, 0, st>>>(d.n1, d.n2, d.x2_ptr, d.x2_src, U, b, f2);
+    launch_pdl(k_forward_x2, dim3(ceil_div(3 * (int64_t)d.n2, 256)), dim3(256), 0, st, d.n1, d.n2,
+               (const int*)d.x2_ptr, (const int*)d.x2_src, (const double*)U, b, f2);
     if (launches) ++*launches;
   }
 }
@@ -1157,25 +1426,28 @@ void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, do
                                                                 d.rows, y, d.VZ, d.P, XF);
     if (launches) ++*launches;
   }
+  if (!d.flow && d.nlevels > d.fuse)
+    cudaMemsetAsync(d.bw_chunk_cnt, 0, sizeof(int) * std::max(d.bwr_off[d.nlevels], 1), st);
   for (int l = d.nlevels - 1; l >= d.fuse && !d.flow; --l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
-    k_bw_gather<<<ceil_div(T.npos, 256), 256, 0, st>>>(d.lvl_pos + T.pos_off, T.npos, d.pos_owner, d.rows, y, XF,
-                                                       d.VZ);
     const int nt = d.bwt_off[l + 1] - d.bwt_off[l];
-    const int nr = d.bwr_off[l + 1] - d.bwr_off[l];
     const int nw = d.bww_off[l + 1] - d.bww_off[l];
-    if (nt) {
-      k_bw_tile<<<nt, 256, 0, st>>>(d.sn, d.M, d.VZ, d.bw_tiles + d.bwt_off[l], d.P);
-      k_bw_reduce<<<ceil_div((int64_t)nr * BT_COLS * 3, 256), 256, 0, st>>>(d.sn, d.bw_chunks + d.bwr_off[l], nr, d.P,
-                                                                            XF);
-    }
-    if (nw) k_backward_warp<<<(nw + 7) / 8, 256, 0, st>>>(d.sn, d.M, d.VZ, d.bw_warp + d.bww_off[l], nw, XF);
-    if (launches) *launches += 1 + 2 * (nt > 0) + (nw > 0);
+    if (nt + nw == 0) continue;
+    if (nt)
+      launch_pdl(k_bw_level, dim3(nt), dim3(256), sizeof(double) * 3 * T.bw_rows, st, (const SnDev*)d.sn,
+                 (const double*)d.M, (const int4*)(d.bw_tiles + d.bwt_off[l]), T.bw_rows,
+                 (const int*)(d.bw_tile_chunk + d.bwt_off[l]), (const int4*)d.bw_chunks, d.bw_chunk_cnt,
+                 (const int*)d.pos_owner, (const int*)d.rows, y, d.P, XF);
+    if (nw)
+      launch_pdl(k_bw_level_warp, dim3((nw + 7) / 8), dim3(256), 0, st, (const SnDev*)d.sn, (const double*)d.M,
+                 (const int*)(d.bw_warp + d.bww_off[l]), nw, (const int*)d.pos_owner, (const int*)d.rows, y, XF);
+    if (launches) *launches += (nt > 0) + (nw > 0);
   }
   if (d.fuse > 0) {
-    k_subtree_backward<<<d.ngroups, SUB_THREADS, 0, st>>>(d.sn, d.M, d.sub_pos, d.sub_pos_off, d.sub_bw,
-                                                          d.sub_bw_off, d.fuse, d.pos_owner, d.rows, y, d.VZ, XF);
+    launch_pdl(k_subtree_backward, dim3(d.ngroups), dim3(SUB_THREADS), 0, st, (const SnDev*)d.sn,
+               (const double*)d.M, (const int*)d.sub_pos, (const int*)d.sub_pos_off, (const int2*)d.sub_bw,
+               (const int*)d.sub_bw_off, d.fuse, (const int*)d.pos_owner, (const int*)d.rows, y, d.VZ, XF);
     if (launches) ++*launches;
   }
 }
