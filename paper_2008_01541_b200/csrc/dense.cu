@@ -341,7 +341,7 @@ __device__ __forceinline__ void upd_block2(double* S, int o, int rbA, int cbA, b
 // warps 1-7 apply the rest of the rank-16 trailing update, so the sequential
 // 16-pivot kernels overlap the update work (2 consumer barriers per block).
 __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
-                                   int* info, int wr, int wc, int lane) {
+                                   int* info, int* flag, int wr, int wc, int lane) {
   const int tid = threadIdx.x, warp = tid >> 5;
   POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
@@ -411,11 +411,21 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
     cons_sync();
     POTRF_MARK(3 + 2 * kb)
   }
-  // L_jj (strict upper zeroed) and L_jj^-T to global (swizzled tiles)
+  // L_jj^-T first (the next tasks read only it: the kernel never reads the
+  // diagonal L tiles), publish, then L_jj (strict upper zeroed)
+  for (int q = tid; q < 64 * 64; q += NCONS) {
+    const int r = q >> 6, c = q & 63;
+    gLinvT[swz(r, c)] = S[(64 + r) * LSP + c];
+  }
+  if (flag) {
+    fence_proxy_async_global();
+    __threadfence();
+    cons_sync();
+    if (tid == 0) st_release(flag, 1);
+  }
   for (int q = tid; q < 64 * 64; q += NCONS) {
     const int r = q >> 6, c = q & 63;
     gL[swz(r, c)] = (c <= r) ? S[r * LSP + c] : 0.0;
-    gLinvT[swz(r, c)] = S[(64 + r) * LSP + c];
   }
   POTRF_MARK(14)
 }
@@ -490,9 +500,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
           fill(d.L + (size_t)tidx(j, k) * TILE, nullptr, 0);
         }
         if (j > 0) {
+          // the partial is usually ready long before diag j-1: only the
+          // 32 KB inv(L_{j-1,j-1})^T transfer waits on the chain
           wait_ready(d.flags + tidx(j, j - 1), 1);
+          fill(d.L + (size_t)tidx(j, j - 1) * TILE, nullptr, 0);
           wait_ready(d.flags + tidx(j - 1, j - 1), 1);
-          fill(d.L + (size_t)tidx(j, j - 1) * TILE, d.LinvT + (size_t)(j - 1) * TILE, 0);
+          fill(d.LinvT + (size_t)(j - 1) * TILE, nullptr, 1);
         }
       } else {
         for (int k = 0; k < j; ++k) {
@@ -536,30 +549,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
         // ---- finalize the sub-diagonal tile on the critical chain:
         // L(j, j-1) = partial * inv(L_{j-1,j-1})^T, publish it (flag 2), and
         // apply its rank-64 update here; diag(j-1) -> diag(j) crosses one flag
-        s = it % NSTAGE;
-        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+        const int sa = it % NSTAGE;  // slot 0: the partial sum
+        mbar_wait(&sm.full[sa], (it / NSTAGE) & 1);
+        ++it;
+        const int sb = it % NSTAGE;  // slot 1: inv(L_{j-1,j-1})^T
+        mbar_wait(&sm.full[sb], (it / NSTAGE) & 1);
+        ++it;
         Acc out;
         acc_zero(out);
-        mma_ab(out, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
-        acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
-        cons_sync();  // every warp has finished reading the stage
-        double* scratch = sm.slot(s, 0);
+        mma_ab(out, sm.slot(sa, 0), sm.slot(sb, 1), wr, wc, lane);
+        cons_sync();  // every warp has finished reading both stages
+        double* scratch = sm.slot(sa, 0);
         acc_to_swz(out, scratch, wr, wc, lane);
-        fence_proxy_async_global();
+        acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+        cons_sync();
+        mma_abt<true>(acc, scratch, scratch, wr, wc, lane);  // its rank-64 update first ...
+        fence_proxy_async_global();                          // ... then publish (the fence overlapped it)
         __threadfence();
         cons_sync();
         if (tid == 0) st_release(d.flags + tidx(j, j - 1), 2);
-        mma_abt<true>(acc, scratch, scratch, wr, wc, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
-        ++it;
+        if (lane == 0) {
+          mbar_arrive(&sm.empty[sa]);
+          mbar_arrive(&sm.empty[sb]);
+        }
       }
       // ---- finalize
       if (d.trace && tid == 0) t_kdone = globaltimer();
       if (i == j) {
         // the whole stage area is idle until the next task: augmented panel + D^-T
         potrf_blocked_tile(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
-                           d.LinvT + (size_t)j * TILE, j, d.info, wr, wc, lane);
+                           d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane);
       } else if (i == j + 1 && !rhs) {
         // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
         acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
