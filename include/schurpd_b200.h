@@ -185,6 +185,15 @@ int32_t spb_ctx_set_state(spb_ctx *ctx, const double *x, const double *R, const 
                           const double *target, const double *f_tilde2, const double *u2_accum);
 /* One frame of solve_frame_schur on the context's state. */
 int32_t spb_ctx_step(spb_ctx *ctx, const spb_step_config *cfg, spb_frame_metrics *metrics);
+/* One whole frame in one call (what Simulation.step does per frame,
+ * harness.py:592-596 -> solver.py:387-455): upload the pose (attachment
+ * targets, posed colliders) and the state (x, active, target), run the frame
+ * (CUDA graph), download x / active / target in place and f_tilde2 / u2_accum,
+ * fill the metrics; one stream synchronisation. R/Q stay on the device
+ * (spb_ctx_get_state pulls them). */
+int32_t spb_ctx_frame(spb_ctx *ctx, const double *att_targets, int32_t num_colliders,
+                      const spb_posed_collider *colliders, double *x, uint8_t *active, double *target,
+                      const spb_step_config *cfg, double *f_tilde2, double *u2_accum, spb_frame_metrics *metrics);
 /* Download state; any pointer may be NULL to skip that field. */
 int32_t spb_ctx_get_state(spb_ctx *ctx, double *x, double *R, double *Q, uint8_t *active, double *target,
                           double *f_tilde2, double *u2_accum);

@@ -94,6 +94,7 @@ _SIGS = {
     "spb_ctx_set_pose": ([P, P, I32, P], I32),
     "spb_ctx_set_state": ([P, P, P, P, P, P, P, P], I32),
     "spb_ctx_step": ([P, P, P], I32),
+    "spb_ctx_frame": ([P, P, I32, P, P, P, P, P, P, P, P], I32),
     "spb_ctx_get_state": ([P, P, P, P, P, P, P, P], I32),
     "spb_ctx_bench": ([P, P, I32, P, P], I32),
     "spb_ctx_bench_cholesky": ([P, I32, P], I32),

@@ -206,7 +206,7 @@ static bool host_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-static int io_upload(Ctx* c, const IoList& l) {
+static int io_upload(Ctx* c, const IoList& l, bool sync = true) {
   TRY(c->io_reserve(l.total));
   size_t off = 0;
   for (int i = 0; i < l.n; ++i) {
@@ -219,7 +219,7 @@ static int io_upload(Ctx* c, const IoList& l) {
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
   // the caller may reuse its buffers as soon as we return
-  SPB_CUDA(cudaStreamSynchronize(c->st));
+  if (sync) SPB_CUDA(cudaStreamSynchronize(c->st));
   return SPB_OK;
 }
 
@@ -437,7 +437,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   TRY(p_part.zeros(2 * (size_t)std::max(p_blocks, 1)));
   TRY(r_part.zeros(2 * (size_t)std::max(r_blocks, 1)));
   TRY(metrics_out.zeros(4));
-  SPB_CUDA(cudaMallocHost(&metrics_host, sizeof(double) * 4));
+  SPB_CUDA(cudaMallocHost(&metrics_host, sizeof(double) * 5));  // 4 metrics + the info word
   SPB_CUDA(cudaDeviceSynchronize());
   return SPB_OK;
 }
@@ -602,17 +602,15 @@ int32_t spb_ctx_add_shape(spb_ctx* cp, const spb_shape_desc* d, int32_t* shape_i
   SPB_GUARD_END
 }
 
-int32_t spb_ctx_set_pose(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols) {
-  SPB_GUARD_BEGIN
-  Ctx* c = reinterpret_cast<Ctx*>(cp);
-  SPB_CUDA(cudaSetDevice(c->device));
+// Pose upload through the pinned staging buffers; the stream must be idle
+// (nothing in flight still reading them).
+static int pose_upload(Ctx* c, const double* att_targets, int32_t ncol, const spb_posed_collider* cols) {
   if (ncol > spb::MAX_COLLIDERS) { spb::set_error("too many colliders"); return SPB_ERR_ARG; }
   if (c->na > 0 && att_targets) {
     memcpy(c->att_tgt_host, att_targets, sizeof(double) * 3 * c->na);
     SPB_CUDA(cudaMemcpyAsync(c->att_tgt.p, c->att_tgt_host, sizeof(double) * 3 * c->na, cudaMemcpyHostToDevice,
                              c->st));
   }
-  SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
   c->cols_host->n = ncol;
   for (int i = 0; i < ncol; ++i) {
     if (cols[i].shape < 0 || cols[i].shape >= (int)c->shapes.size()) {
@@ -626,6 +624,14 @@ int32_t spb_ctx_set_pose(spb_ctx* cp, const double* att_targets, int32_t ncol, c
   TRY(c->sync_shapes());
   SPB_CUDA(cudaMemcpyAsync(c->cols_dev.p, c->cols_host, sizeof(spb::ColliderSet), cudaMemcpyHostToDevice, c->st));
   return SPB_OK;
+}
+
+int32_t spb_ctx_set_pose(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
+  return pose_upload(c, att_targets, ncol, cols);
   SPB_GUARD_END
 }
 
@@ -705,23 +711,45 @@ static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
   return c->enqueue_frame(outer, inner, cad, ev);
 }
 
+// Enqueue one frame and the metrics read-back; no synchronisation.
+static int frame_enqueue(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
+  if (cfg->outer_iters < 1 || cfg->inner_iters < 1) { spb::set_error("outer_iters and inner_iters must be >= 1"); return SPB_ERR_ARG; }
+  if (c->n2 > 0) SPB_CUDA(cudaMemsetAsync(c->info.p, 0, sizeof(int), c->st));
+  TRY(run_frame(c, cfg, ev));
+  SPB_CUDA(cudaMemcpyAsync(c->metrics_host, c->metrics_out.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
+  int* info_h = reinterpret_cast<int*>(c->metrics_host + 4);
+  *info_h = 0;
+  if (c->n2 > 0) SPB_CUDA(cudaMemcpyAsync(info_h, c->info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  return SPB_OK;
+}
+
+// After the stream has drained: metrics out, SPB_ERR_INDEFINITE on a bad pivot.
+static int frame_finish(Ctx* c, spb_frame_metrics* m) {
+  m->energy = c->metrics_host[0];
+  m->max_penetration = c->metrics_host[1];
+  m->residual = c->residual_valid ? c->metrics_host[2] : 0.0;
+  m->active_proxies = (int64_t)llround(c->metrics_host[3]);
+  m->kernel_launches = c->last_launches;
+  const int info_h = *reinterpret_cast<const int*>(c->metrics_host + 4);
+  if (info_h > 0) {
+    m->info = info_h - 1;
+    spb::set_error("dense factorization failed: non-positive pivot");
+    return SPB_ERR_INDEFINITE;
+  }
+  return SPB_OK;
+}
+
 int32_t spb_ctx_step(spb_ctx* cp, const spb_step_config* cfg, spb_frame_metrics* m) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);
   SPB_CUDA(cudaSetDevice(c->device));
-  if (cfg->outer_iters < 1 || cfg->inner_iters < 1) { spb::set_error("outer_iters and inner_iters must be >= 1"); return SPB_ERR_ARG; }
   auto t0 = std::chrono::steady_clock::now();
   memset(m, 0, sizeof(*m));
-  if (c->n2 > 0) SPB_CUDA(cudaMemsetAsync(c->info.p, 0, sizeof(int), c->st));
   cudaEvent_t ev[6];
   bool timed = !cfg->use_graph;
   if (timed)
     for (auto& e : ev) SPB_CUDA(cudaEventCreate(&e));
-  int rc = run_frame(c, cfg, timed ? ev : nullptr);
-  if (rc != SPB_OK) return rc;
-  SPB_CUDA(cudaMemcpyAsync(c->metrics_host, c->metrics_out.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
-  int info_h = 0;
-  if (c->n2 > 0) SPB_CUDA(cudaMemcpyAsync(&info_h, c->info.p, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  TRY(frame_enqueue(c, cfg, timed ? ev : nullptr));
   SPB_CUDA(cudaStreamSynchronize(c->st));
   if (timed) {
     float a;
@@ -731,18 +759,38 @@ int32_t spb_ctx_step(spb_ctx* cp, const spb_step_config* cfg, spb_frame_metrics*
     cudaEventElapsedTime(&a, ev[3], ev[4]); m->t_backward_ms = a;
     for (auto& e : ev) cudaEventDestroy(e);
   }
-  m->energy = c->metrics_host[0];
-  m->max_penetration = c->metrics_host[1];
-  m->residual = c->residual_valid ? c->metrics_host[2] : 0.0;
-  m->active_proxies = (int64_t)llround(c->metrics_host[3]);
-  m->kernel_launches = c->last_launches;
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  if (info_h > 0) {
-    m->info = info_h - 1;
-    spb::set_error("dense factorization failed: non-positive pivot");
-    return SPB_ERR_INDEFINITE;
-  }
-  return SPB_OK;
+  return frame_finish(c, m);
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
+                      double* x, uint8_t* active, double* target, const spb_step_config* cfg, double* f_tilde2,
+                      double* u2_accum, spb_frame_metrics* m) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  auto t0 = std::chrono::steady_clock::now();
+  memset(m, 0, sizeof(*m));
+  SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
+  TRY(pose_upload(c, att_targets, ncol, cols));
+  IoList up;
+  up.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  if (c->P) up.add(c->active.p, active, c->P);
+  if (c->P) up.add(c->target.p, target, sizeof(double) * 3 * c->P);
+  TRY(io_upload(c, up, false));
+  TRY(frame_enqueue(c, cfg, nullptr));
+  IoList down;
+  down.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  if (c->P) down.add(c->active.p, active, c->P);
+  if (c->P) down.add(c->target.p, target, sizeof(double) * 3 * c->P);
+  if (c->n2) down.add(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2);
+  if (c->n2) down.add(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2);
+  // the staging area is shared by the upload and the download: the download
+  // lands behind the upload's copies in stream order, so one sync covers both
+  TRY(io_download(c, down));
+  m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return frame_finish(c, m);
   SPB_GUARD_END
 }
 
