@@ -121,6 +121,16 @@ def replica_throughput(world: int, ms_per_frame_max: float) -> float:
     return world * 1e3 / ms_per_frame_max
 
 
+def measured_hbm_peak():
+    """HBM GB/s from the driver-written MEASURED_PEAKS.json, else the
+    profiling guide's B200 figure."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
+    except Exception:
+        return 6552.3, "fallback (no MEASURED_PEAKS.json on this box)"
+
+
 def committed_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum of one k_cholesky_tiles
     launch from the newest committed `ncu --set full` capture (profiles/)."""
@@ -283,6 +293,22 @@ def run_b200(args):
         return
     fp64_peak = measure_fp64_peak()
     traffic, traffic_src = committed_traffic()
+    # per-piece graph-replay times -> achieved HBM GB/s of the solves (north_star (4))
+    kms = {}
+    for name, which in (("cholesky", 0), ("dense_backward", 1), ("sigma0_gemv", 2), ("sparse_forward", 3),
+                        ("sparse_backward", 4)):
+        v = ctypes.c_double(0)
+        _native.check(lib.spb_ctx_bench_kernel(ds.handle, which, 10, ctypes.byref(v)))
+        kms[name] = v.value
+    f = sim.system.factor.native
+    panel_bytes = 8.0 * f.panel_values
+    tri_bytes = 8.0 * m * (m + 1) / 2  # one triangle of L or sigma0, FP64
+    hbm_peak, hbm_src = measured_hbm_peak()
+    gbs = lambda b, ms: b / (ms * 1e-3) / 1e9 if ms > 0 else None  # noqa: E731
+    ne, nalpha = sim.mesh.num_elements, len(sim.partition.e_alpha)
+    bytes_frame = 2 * panel_bytes + 4 * tri_bytes + 360.0 * nalpha + 264.0 * ne
+    t_fp64 = chol_flops / (fp64_peak * 1e12) * 1e3
+    t_hbm = bytes_frame / (hbm_peak * 1e9) * 1e3
     achieved = chol_flops / (chol.value * 1e-3) / 1e12
     line = {
         "metric": "PD frames/sec w/ collisions (600K tets, 5% collision DOFs); Cholesky FP64 TFLOPS",
@@ -299,6 +325,17 @@ def run_b200(args):
                      "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
                      "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (MEASURED_PEAKS.json has no FP64)",
                      "flops_per_launch": chol_flops},
+        "kernels_ms": kms,
+        "hbm_gbs": {"sparse_forward": gbs(panel_bytes, kms["sparse_forward"]),
+                    "sparse_backward": gbs(panel_bytes, kms["sparse_backward"]),
+                    "dense_backward": gbs(tri_bytes, kms["dense_backward"]),
+                    "sigma0_gemv": gbs(tri_bytes, kms["sigma0_gemv"]),
+                    "peak": hbm_peak, "peak_source": hbm_src,
+                    "bytes": {"panels_per_sweep": panel_bytes, "triangle": tri_bytes}},
+        "frame_roofline": {"t_fp64_ms": t_fp64, "t_hbm_ms": t_hbm, "bytes_per_frame": bytes_frame,
+                           "t_roofline_ms": t_fp64 + t_hbm, "frac": (t_fp64 + t_hbm) / ms_frame,
+                           "note": "m^3/3 at the live DGEMM peak + algorithmic bytes (2 sweeps of panels, "
+                                   "4 triangle passes, element and metric passes) at the HBM peak"},
         "gpu_launches": launches, "setup_s": setup_s,
         "clocks": clk.summary(),
     }

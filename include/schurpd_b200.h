@@ -205,6 +205,10 @@ int32_t spb_ctx_bench(spb_ctx *ctx, const spb_step_config *cfg, int32_t frames, 
 int32_t spb_ctx_trace_cholesky(spb_ctx *ctx, uint64_t *out, int32_t *tasks_out, int32_t *ntasks);
 /* Cholesky-only timing on the context's current H (tile kernel), ms per launch. */
 int32_t spb_ctx_bench_cholesky(spb_ctx *ctx, int32_t reps, double *ms);
+/* Graph-replay mean time of one piece of the frame on the current buffers:
+ * 0 tile Cholesky, 1 dense backward solve, 2 sigma0 mat-vec, 3 sparse forward
+ * sweep, 4 sparse backward sweep (bench.py rooflines). */
+int32_t spb_ctx_bench_kernel(spb_ctx *ctx, int32_t which, int32_t reps, double *ms);
 
 /* ------------------------------------------------------- one-shot ops */
 int32_t spb_op_deformation_gradients(int64_t ne, const int64_t *tets, const double *dm_inverse, int64_t n,

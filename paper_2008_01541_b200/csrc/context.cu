@@ -852,6 +852,60 @@ int32_t spb_ctx_trace_cholesky(spb_ctx* cp, uint64_t* out, int32_t* tasks_out, i
   SPB_GUARD_END
 }
 
+// Graph-replay timing of one piece of the frame on the context's current
+// buffers (diagnostics / bench.py rooflines): 0 tile Cholesky, 1 dense
+// backward, 2 sigma0 GEMV + reduce, 3 sparse forward sweep, 4 sparse backward sweep.
+int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* ms) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  *ms = 0;
+  if (which < 0 || which > 4) { spb::set_error("unknown kernel id"); return SPB_ERR_ARG; }
+  if ((which <= 2 && c->n2 == 0) || (which >= 3 && c->n1 == 0)) return SPB_OK;
+  SPB_CUDA(cudaSetDevice(c->device));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  cudaGraph_t g;
+  SPB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+  switch (which) {
+    case 0:
+      cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st);
+      cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st);
+      spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
+      break;
+    case 1: spb::launch_dense_backward(c->st, c->dd, c->xrows.p, c->u2.p); break;
+    case 2:
+      spb::launch_sym_tile_gemv(c->st, c->dd, c->u2.p, c->gemv_partial.p);
+      spb::launch_sym_tile_gemv_reduce(c->st, c->dd, c->gemv_partial.p, c->s0u.p);
+      break;
+    case 3: spb::sparse_forward(c->st, *c->factor->dev, c->b.p, c->y.p, c->U.p, c->f_tilde2.p, nullptr); break;
+    case 4: spb::sparse_backward(c->st, *c->factor->dev, c->y.p, c->XF.p, nullptr); break;
+  }
+  cudaError_t ce = cudaStreamEndCapture(c->st, &g);
+  if (ce != cudaSuccess) { spb::set_error(std::string("capture: ") + cudaGetErrorString(ce)); return SPB_ERR_CUDA; }
+  cudaGraphExec_t ge;
+  SPB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  cudaGraphDestroy(g);
+  cudaEvent_t e0, e1;
+  SPB_CUDA(cudaEventCreate(&e0));
+  SPB_CUDA(cudaEventCreate(&e1));
+  SPB_CUDA(cudaGraphLaunch(ge, c->st));  // warm-up
+  float tot = 0;
+  for (int r = 0; r < std::max(reps, 1); ++r) {
+    SPB_CUDA(cudaEventRecord(e0, c->st));
+    SPB_CUDA(cudaGraphLaunch(ge, c->st));
+    SPB_CUDA(cudaEventRecord(e1, c->st));
+    SPB_CUDA(cudaEventSynchronize(e1));
+    float a;
+    SPB_CUDA(cudaEventElapsedTime(&a, e0, e1));
+    tot += a;
+  }
+  *ms = tot / std::max(reps, 1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
 int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);
