@@ -807,6 +807,25 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
 }
 
 // sigma0 u: per lower tile, the row and (off-diagonal) column contributions.
+// Thread (row group g, column c) loads its 16 tile entries once (coalesced
+// across c), forms the column part in registers and the row part with one
+// 16-way warp transpose-sum per RHS; fixed-order shared reductions finish both.
+__device__ __forceinline__ double gemv_transpose_sum16(double (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    const bool upper = lane & off;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const double send = upper ? v[i] : v[i + off];
+      const double keep = upper ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];  // lane l: the total of entry l % 16
+}
+
 __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double* __restrict__ u,
                                                         double* __restrict__ partial) {
   const int t = blockIdx.x;
@@ -816,60 +835,76 @@ __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double
   const int j = t - tidx(i, 0);
   __shared__ double ui[3 * TS], uj[3 * TS];
   __shared__ double colred[4][3 * TS];
-  const int tid = threadIdx.x;
+  __shared__ double rowred[2][3 * TS];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int c = tid & 63, g = tid >> 6;
   const int m = d.m;
   if (tid < TS) {
-    int ri = i * TS + tid, rj = j * TS + tid;
+    const int ri = i * TS + tid, rj = j * TS + tid;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       ui[q * TS + tid] = ri < m ? u[3 * ri + q] : 0.0;
       uj[q * TS + tid] = rj < m ? u[3 * rj + q] : 0.0;
     }
   }
-  __syncthreads();
   const double* T = d.sigma0 + (size_t)t * TILE;
-  const int lane = tid & 31, w = tid >> 5;
+  double a[16];
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) a[rr] = T[swz(16 * g + rr, c)];
+  __syncthreads();
   double* out_row = partial + (size_t)t * 6 * TS;
   double* out_col = out_row + 3 * TS;
-  for (int rr = 0; rr < 8; ++rr) {
-    int row = w * 8 + rr;
-    double a0 = T[swz(row, lane)], a1 = T[swz(row, lane + 32)];
-    double s0 = a0 * uj[lane] + a1 * uj[lane + 32];
-    double s1 = a0 * uj[TS + lane] + a1 * uj[TS + lane + 32];
-    double s2 = a0 * uj[2 * TS + lane] + a1 * uj[2 * TS + lane + 32];
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    if (lane == 0) {
-      out_row[row] = s0;
-      out_row[TS + row] = s1;
-      out_row[2 * TS + row] = s2;
-    }
+  // row part: sum over c of a[r][c] uj[c]; warps hold 32 columns x 16 rows
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double w = uj[q * TS + c];
+    double v[16];
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) v[rr] = a[rr] * w;
+    const double sum = gemv_transpose_sum16(v, lane);
+    if (lane < 16) rowred[c >> 5][q * TS + 16 * g + lane] = sum;
   }
   if (i != j) {
-    const int cc = tid & 63, grp = tid >> 6;
-    double s0 = 0, s1 = 0, s2 = 0;
-    for (int rr = grp * 16; rr < grp * 16 + 16; ++rr) {
-      double a = T[swz(rr, cc)];
-      s0 += a * ui[rr];
-      s1 += a * ui[TS + rr];
-      s2 += a * ui[2 * TS + rr];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) s += a[rr] * ui[q * TS + 16 * g + rr];
+      colred[g][q * TS + c] = s;
     }
-    colred[grp][cc] = s0;
-    colred[grp][TS + cc] = s1;
-    colred[grp][2 * TS + cc] = s2;
-    __syncthreads();
-    if (tid < 3 * TS) out_col[tid] = ((colred[0][tid] + colred[1][tid]) + colred[2][tid]) + colred[3][tid];
+  }
+  __syncthreads();
+  if (tid < 3 * TS) {
+    out_row[tid] = rowred[0][tid] + rowred[1][tid];
+    if (i != j) out_col[tid] = ((colred[0][tid] + colred[1][tid]) + colred[2][tid]) + colred[3][tid];
   }
 }
 
+// out[b] = sum over the tiles of block row/column b, in fixed order (loads
+// unrolled so they are in flight together; the adds stay sequential)
 __global__ void k_sym_gemv_reduce(DenseDev d, const double* __restrict__ partial, double* __restrict__ out) {
   const int b = blockIdx.x, tid = threadIdx.x;
   if (tid >= 3 * TS) return;
   const int q = tid / TS, r = tid % TS;
   double s = 0.0;
-  for (int j = 0; j <= b; ++j) s += partial[(size_t)tidx(b, j) * 6 * TS + q * TS + r];
-  for (int i = b + 1; i < d.N; ++i) s += partial[(size_t)tidx(i, b) * 6 * TS + 3 * TS + q * TS + r];
+  int j = 0;
+  for (; j + 8 <= b + 1; j += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = partial[(size_t)tidx(b, j + k) * 6 * TS + q * TS + r];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; j <= b; ++j) s += partial[(size_t)tidx(b, j) * 6 * TS + q * TS + r];
+  int i = b + 1;
+  for (; i + 8 <= d.N; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = partial[(size_t)tidx(i + k, b) * 6 * TS + 3 * TS + q * TS + r];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; i < d.N; ++i) s += partial[(size_t)tidx(i, b) * 6 * TS + 3 * TS + q * TS + r];
   int row = b * TS + r;
   if (row < d.m) out[3 * row + q] = s;
 }
