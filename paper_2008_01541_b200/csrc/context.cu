@@ -841,7 +841,9 @@ int32_t spb_ctx_trace_cholesky(spb_ctx* cp, uint64_t* out, int32_t* tasks_out, i
   SPB_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * 4 * c->ntasks));
   spb::DenseDev dd = c->dd;
   dd.trace = tr;
-  SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
+  const char* nd = getenv("SPB_CHOL_NODEPS");  // diagnostics: no dependency waits
+  SPB_CUDA(cudaMemsetAsync(c->flags.p, (nd && nd[0] == '1') ? 2 : 0,
+                           sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
   SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
   spb::launch_cholesky_tiles(c->st, dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
   SPB_CUDA(cudaStreamSynchronize(c->st));

@@ -38,21 +38,21 @@ constexpr int LDP = 66;                  // plain row stride of the potrf scratc
 __host__ __device__ __forceinline__ int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
 int dense_tile_count(int N) { return N * (N + 1) / 2; }
 
-// dynamic smem: [stage s][slot a/b] padded tiles, then col[2][128], ipiv[2],
-// then the mbarriers and the task slot
+// dynamic smem: [stage s][slot a/b] swizzled tiles, a finalize scratch tile,
+// then the stage mbarriers, the task-ring mbarriers and the 2 task slots
 constexpr int SM_STAGES = NSTAGE * 2 * PTILE;
-constexpr int SM_COL = SM_STAGES;
-constexpr int SM_IPIV = SM_COL + 2 * 128;
-constexpr int SM_BAR = SM_IPIV + 2;  // in doubles (8-byte aligned)
-size_t cholesky_smem_bytes() { return sizeof(double) * (SM_BAR + 2 * NSTAGE + 1); }
+constexpr int SM_SCR = SM_STAGES;
+constexpr int SM_BAR = SM_SCR + PTILE;  // in doubles (8-byte aligned)
+size_t cholesky_smem_bytes() { return sizeof(double) * (SM_BAR + 2 * NSTAGE + 4 + 1); }
 
 struct CholSmem {
   double* stage0;
-  double* col;                // [2][128]
-  double* ipiv;               // [2]
+  double* scratch;            // one tile: regular-tile finalize
   unsigned long long* full;   // [NSTAGE]
   unsigned long long* empty;  // [NSTAGE]
-  int* task;
+  unsigned long long* tfull;  // [2] task ring: the producer published a task id
+  unsigned long long* tempty; // [2] task ring: every consumer warp read it
+  int* task;                  // [2]
   __device__ __forceinline__ double* slot(int s, int k) const { return stage0 + (s * 2 + k) * PTILE; }
 };
 
@@ -431,16 +431,22 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
 }
 
 // ---------------------------------------------------------------- kernel
+// The producer warp runs one task ahead: it claims task t+1 and streams its
+// tiles while the consumers finalize task t (task ids pass through a 2-slot
+// mbarrier ring), so claim latency, the first tile's TMA latency and the
+// finalize overlap. Diagonal tasks factor in the stage area, so across them
+// the producer waits for the consumers (named barrier 2).
 __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, const int2* __restrict__ tasks,
                                                                 int ntasks) {
   extern __shared__ __align__(128) double smd[];
   CholSmem sm;
   sm.stage0 = smd;
-  sm.col = smd + SM_COL;
-  sm.ipiv = smd + SM_IPIV;
+  sm.scratch = smd + SM_SCR;
   sm.full = reinterpret_cast<unsigned long long*>(smd + SM_BAR);
   sm.empty = sm.full + NSTAGE;
-  sm.task = reinterpret_cast<int*>(sm.empty + NSTAGE);
+  sm.tfull = sm.empty + NSTAGE;
+  sm.tempty = sm.tfull + 2;
+  sm.task = reinterpret_cast<int*>(sm.tempty + 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool producer = warp == 8;
   const int wr = warp >> 2, wc = warp & 3;
@@ -451,45 +457,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], NCONS / 32);
     }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&sm.tfull[k], 1);
+      mbar_init(&sm.tempty[k], NCONS / 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   int it = 0;  // stage-use counter, advanced identically by producer and consumers
-  unsigned long long t_claim = 0, t_kdone = 0, t_fin = 0;
-  for (;;) {
-    if (tid == 0) *sm.task = atomicAdd(d.counter, 1);
-    __syncthreads();
-    const int task = *sm.task;
-    if (task >= ntasks) break;
-    const int2 ij = tasks[task];
-    const int i = ij.x, j = ij.y;
-    const bool rhs = (i == N);
-    if (d.trace && tid == 0) t_claim = globaltimer();
-    int* myflag = d.flags + (rhs ? ntiles + j : tidx(i, j));
-
-    if (producer) {
-      // lane 0 polls flags, waits for a free stage and issues one 32 KB bulk
-      // copy (TMA) per tile into the stage ring
-      auto fill = [&](const double* a, const double* b, int slot_a) {
-        const int s = it % NSTAGE;
-        if (lane == 0) {
-          mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
-          mbar_expect_tx(&sm.full[s], (b ? 2 : 1) * TILE_BYTES);
-        }
-        if (lane == 0) {
-          bulk_g2s(sm.slot(s, slot_a), a, TILE_BYTES, &sm.full[s]);
-          if (b) bulk_g2s(sm.slot(s, 1), b, TILE_BYTES, &sm.full[s]);
-        }
-        __syncwarp();
-        ++it;
-      };
-      auto wait_ready = [&](const int* f, int v) {
-        if (lane == 0) poll_flag(f, v);
-        __syncwarp();
-      };
-      // flag values: 1 = final; the sub-diagonal tile (k+1, k) is first
-      // published as a partial sum (1) and finalized by diagonal task k+1 (2)
-      auto tile_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), r == c + 1 ? 2 : 1); };
+  if (producer) {
+    auto fill = [&](const double* a, const double* b, int slot_a) {
+      const int s = it % NSTAGE;
+      if (lane == 0) {
+        mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
+        mbar_expect_tx(&sm.full[s], (b ? 2 : 1) * TILE_BYTES);
+        bulk_g2s(sm.slot(s, slot_a), a, TILE_BYTES, &sm.full[s]);
+        if (b) bulk_g2s(sm.slot(s, 1), b, TILE_BYTES, &sm.full[s]);
+      }
+      __syncwarp();
+      ++it;
+    };
+    auto wait_ready = [&](const int* f, int v) {
+      if (lane == 0) poll_flag(f, v);
+      __syncwarp();
+    };
+    // flag values: 1 = final; the sub-diagonal tile (k+1, k) is first
+    // published as a partial sum (1) and finalized by diagonal task k+1 (2)
+    auto tile_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), r == c + 1 ? 2 : 1); };
+    for (int use = 0;; ++use) {
+      const int k2 = use & 1;
+      int task = 0;
+      if (lane == 0) {
+        task = atomicAdd(d.counter, 1);
+        mbar_wait(&sm.tempty[k2], ((use >> 1) & 1) ^ 1);
+        sm.task[k2] = task;
+        mbar_arrive(&sm.tfull[k2]);  // release: the id is visible to the waiters
+      }
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task >= ntasks) break;
+      const int2 ij = tasks[task];
+      const int i = ij.x, j = ij.y;
+      const bool rhs = (i == N);
       const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
       fill(src, nullptr, 0);
       if (i == j) {
@@ -507,6 +515,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
           wait_ready(d.flags + tidx(j - 1, j - 1), 1);
           fill(d.LinvT + (size_t)(j - 1) * TILE, nullptr, 1);
         }
+        // the factorization uses the whole stage area: no prefetch across it
+        asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");
       } else {
         for (int k = 0; k < j; ++k) {
           if (rhs) wait_ready(d.flags + ntiles + k, 1);
@@ -519,91 +529,105 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
           fill(d.LinvT + (size_t)j * TILE, nullptr, 1);
         }
       }
-    } else {
-      // ---- consumers: acc <- H tile (sigma0 + C22) or the g^T tile
-      Acc acc;
-      int s = it % NSTAGE;
+    }
+    return;
+  }
+  // ---------------------------------------------------------- consumers
+  unsigned long long t_claim = 0, t_kdone = 0, t_fin = 0;
+  for (int use = 0;; ++use) {
+    const int k2 = use & 1;
+    mbar_wait(&sm.tfull[k2], (use >> 1) & 1);
+    const int task = sm.task[k2];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.tempty[k2]);
+    if (task >= ntasks) break;
+    const int2 ij = tasks[task];
+    const int i = ij.x, j = ij.y;
+    const bool rhs = (i == N);
+    if (d.trace && tid == 0) t_claim = globaltimer();
+    int* myflag = d.flags + (rhs ? ntiles + j : tidx(i, j));
+    // ---- acc <- H tile (sigma0 + C22) or the g^T tile
+    Acc acc;
+    int s = it % NSTAGE;
+    mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+    // only tiles holding C22 entries (near the diagonal) need the add + barrier
+    if (!rhs && d.c22_tile_ptr && d.c22_tile_ptr[tidx(i, j)] < d.c22_tile_ptr[tidx(i, j) + 1]) {
+      add_c22(d, tidx(i, j), sm.slot(s, 0));
+      cons_sync();
+    }
+    smem_to_acc(acc, sm.slot(s, 0), wr, wc, lane);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
+    ++it;
+    const int nk = (i == j) ? j - 1 : j;  // the diagonal task's last k comes from the partial
+    for (int k = 0; k < nk; ++k) {
+      // ---- left-looking accumulation
+      s = it % NSTAGE;
       mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-      if (!rhs && d.c22_tile_ptr) {
-        add_c22(d, tidx(i, j), sm.slot(s, 0));
-        cons_sync();
-      }
-      smem_to_acc(acc, sm.slot(s, 0), wr, wc, lane);
-      fence_proxy_async_smem();
+      mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, i == j ? 0 : 1), wr, wc, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
-      int last = s;
       ++it;
-      const int nk = (i == j) ? j - 1 : j;  // the diagonal task's last k comes from the partial
-      for (int k = 0; k < nk; ++k) {
-        // ---- left-looking accumulation
-        s = it % NSTAGE;
-        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-        mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, i == j ? 0 : 1), wr, wc, lane);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
-        last = s;
-        ++it;
-      }
-      if (i == j && j > 0) {
-        // ---- finalize the sub-diagonal tile on the critical chain:
-        // L(j, j-1) = partial * inv(L_{j-1,j-1})^T, publish it (flag 2), and
-        // apply its rank-64 update here; diag(j-1) -> diag(j) crosses one flag
-        const int sa = it % NSTAGE;  // slot 0: the partial sum
-        mbar_wait(&sm.full[sa], (it / NSTAGE) & 1);
-        ++it;
-        const int sb = it % NSTAGE;  // slot 1: inv(L_{j-1,j-1})^T
-        mbar_wait(&sm.full[sb], (it / NSTAGE) & 1);
-        ++it;
-        Acc out;
-        acc_zero(out);
-        mma_ab(out, sm.slot(sa, 0), sm.slot(sb, 1), wr, wc, lane);
-        cons_sync();  // every warp has finished reading both stages
-        double* scratch = sm.slot(sa, 0);
-        acc_to_swz(out, scratch, wr, wc, lane);
-        acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
-        cons_sync();
-        mma_abt<true>(acc, scratch, scratch, wr, wc, lane);  // its rank-64 update first ...
-        fence_proxy_async_global();                          // ... then publish (the fence overlapped it)
-        __threadfence();
-        cons_sync();
-        if (tid == 0) st_release(d.flags + tidx(j, j - 1), 2);
-        if (lane == 0) {
-          mbar_arrive(&sm.empty[sa]);
-          mbar_arrive(&sm.empty[sb]);
-        }
-      }
-      // ---- finalize
-      if (d.trace && tid == 0) t_kdone = globaltimer();
-      if (i == j) {
-        // the whole stage area is idle until the next task: augmented panel + D^-T
-        potrf_blocked_tile(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
-                           d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane);
-      } else if (i == j + 1 && !rhs) {
-        // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
-        acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
-      } else {
-        double* scratch = sm.slot(last, 0);
-        cons_sync();  // every warp has finished reading stage `last`
-        acc_to_swz(acc, scratch, wr, wc, lane);
-        cons_sync();
-        s = it % NSTAGE;
-        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-        Acc out;
-        acc_zero(out);
-        mma_ab(out, scratch, sm.slot(s, 1), wr, wc, lane);  // acc * inv(L_jj)^T = acc * LinvT
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[s]);
-        ++it;
-        double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
-        acc_to_swz(out, dst, wr, wc, lane);
-      }
-      if (d.trace && tid == 0) t_fin = globaltimer();
-      fence_proxy_async_smem();    // generic smem writes before later bulk copies into the stages
-      fence_proxy_async_global();  // generic global tile stores before other CTAs' bulk reads
-      __threadfence();
     }
-    __syncthreads();
+    if (i == j && j > 0) {
+      // ---- finalize the sub-diagonal tile on the critical chain:
+      // L(j, j-1) = partial * inv(L_{j-1,j-1})^T, publish it (flag 2), and
+      // apply its rank-64 update here; diag(j-1) -> diag(j) crosses one flag
+      const int sa = it % NSTAGE;  // slot 0: the partial sum
+      mbar_wait(&sm.full[sa], (it / NSTAGE) & 1);
+      ++it;
+      const int sb = it % NSTAGE;  // slot 1: inv(L_{j-1,j-1})^T
+      mbar_wait(&sm.full[sb], (it / NSTAGE) & 1);
+      ++it;
+      Acc out;
+      acc_zero(out);
+      mma_ab(out, sm.slot(sa, 0), sm.slot(sb, 1), wr, wc, lane);
+      cons_sync();  // every warp has finished reading both stages
+      double* scratch = sm.scratch;
+      acc_to_swz(out, scratch, wr, wc, lane);
+      acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+      cons_sync();
+      mma_abt<true>(acc, scratch, scratch, wr, wc, lane);  // its rank-64 update first ...
+      fence_proxy_async_global();                          // ... then publish (the fence overlapped it)
+      __threadfence();
+      cons_sync();
+      if (tid == 0) st_release(d.flags + tidx(j, j - 1), 2);
+      if (lane == 0) {
+        mbar_arrive(&sm.empty[sa]);
+        mbar_arrive(&sm.empty[sb]);
+      }
+    }
+    // ---- finalize
+    if (d.trace && tid == 0) t_kdone = globaltimer();
+    if (i == j) {
+      // the producer is parked: the whole stage area holds the augmented panel + D^-T
+      potrf_blocked_tile(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
+                         d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane);
+    } else if (i == j + 1 && !rhs) {
+      // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
+      acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
+    } else {
+      // the producer may already be filling stages for the next task: the
+      // finalize works in the dedicated scratch tile
+      acc_to_swz(acc, sm.scratch, wr, wc, lane);
+      cons_sync();
+      s = it % NSTAGE;
+      mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+      Acc out;
+      acc_zero(out);
+      mma_ab(out, sm.scratch, sm.slot(s, 1), wr, wc, lane);  // acc * inv(L_jj)^T = acc * LinvT
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      ++it;
+      double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
+      acc_to_swz(out, dst, wr, wc, lane);
+    }
+    if (d.trace && tid == 0) t_fin = globaltimer();
+    fence_proxy_async_smem();    // generic smem writes before later bulk copies into the stages
+    fence_proxy_async_global();  // generic global tile stores before other CTAs' bulk reads
+    __threadfence();
+    cons_sync();  // every consumer's stores are fenced; the scratch tile is free again
     if (tid == 0) {
       st_release(myflag, 1);
       if (d.trace) {
@@ -614,6 +638,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
         tr[3] = t_fin;
       }
     }
+    if (i == j) asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");  // release the producer
   }
 }
 
