@@ -350,6 +350,86 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_batch(args):
+    """BASELINE config 5: a batch of independent scenes per GPU that share one
+    GlobalSystem (same mesh, attachments, partition: one factor in HBM) and
+    differ in collider speed (SURVEY cfg5: v_k = -0.004 (1 + k/64) m/frame).
+    `value` = whole-job scene-frames/s with every scene's frames stepped
+    concurrently (one stream each); e2e = the same through Simulation.step."""
+    import ctypes
+
+    import paper_2008_01541_b200 as P
+    from paper_2008_01541_b200 import _native
+    from paper_2008_01541_b200.solver import device_scene
+    from scenes import CONFIGS, block_yaml
+
+    rank, world, local = _env_rank()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist_mod
+
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    S = args.scenes
+    t0 = time.perf_counter()
+    sims = []
+    for k in range(S):
+        kk = rank * S + k
+        sim = P.Simulation(P.parse_scenario(block_yaml(*CONFIGS[args.config], vel=-0.004 * (1 + kk / 64.0),
+                                                       outer=args.outer, inner=args.inner)), diagnostics=False)
+        if sims:
+            sim.system = sims[0].system  # one factor for the batch (same mesh and partition)
+        sims.append(sim)
+    setup_s = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        for sim in sims:
+            sim.step()
+    handles = (ctypes.c_void_p * S)(*[device_scene(sm.model, sm.system).handle for sm in sims])
+    cfg = _native.StepConfig(args.outer, args.inner, _native.CADENCES[sims[0].config.detection_cadence], 1, 0, -1.0)
+    lib = _native.lib()
+    ms = ctypes.c_double(0)
+    clk = ClockSampler(local)
+    clk.__enter__()
+    if dist is not None:
+        dist.barrier()
+    _native.check(lib.spb_bench_batch(handles, S, ctypes.byref(cfg), args.steps, ctypes.byref(ms)))
+    one = ctypes.c_double(0)
+    _native.check(lib.spb_ctx_bench(handles[0], ctypes.byref(cfg), args.steps, ctypes.byref(one), None))
+    if dist is not None:
+        dist.barrier()
+    te = time.perf_counter()
+    for _ in range(max(1, args.steps // 4)):
+        for sim in sims:
+            sim.step()
+    e2e_s = (time.perf_counter() - te) / max(1, args.steps // 4)
+    clk.__exit__(None, None, None)
+    ms_round = max_over_ranks(dist, ms.value)
+    e2e_s = max_over_ranks(dist, e2e_s)
+    if rank == 0:
+        n, P_ = sims[0].mesh.num_nodes, len(sims[0].model.proxies)
+        m = sims[0].partition.n2
+        line = {
+            "metric": f"scene-frames/sec, batch of {S * world} independent {sims[0].mesh.num_elements // 1000}K-tet "
+                      f"scenes ({S} per GPU, one shared factor per GPU)",
+            "value": world * S * 1e3 / ms_round, "unit": "scene-frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_round, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (lattice scenes through the reference schema)",
+            "config": {"workload": f"{args.config} batch: {S} scenes/GPU, {sims[0].mesh.num_elements} tets, "
+                                   f"{n} nodes, m={m}, {P_} proxies each", "scenes_per_gpu": S,
+                       "single_scene_ms_per_frame": one.value,
+                       "batch_speedup_vs_serial": S * one.value / ms_round,
+                       "parallelism": f"{S} concurrent contexts x {world} GPU(s), no collective"},
+            "e2e": {"value": world * S / e2e_s, "unit": "scene-frames/s",
+                    "h2d_bytes_per_step": S * (24 * n + P_ + 24 * P_), "d2h_bytes_per_step": S * (24 * n + P_ + 24 * P_ + 48 * m)},
+            "setup_s": setup_s, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def met_launches(ds, cfg):
     import ctypes
 
@@ -373,11 +453,14 @@ def main():
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--ref-frames", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scenes", type=int, default=1, help="batch mode: concurrent scenes per GPU (cfg5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.scenes > 1:
+        run_batch(args)
     else:
         run_b200(args)
 

@@ -209,6 +209,11 @@ int32_t spb_ctx_bench_cholesky(spb_ctx *ctx, int32_t reps, double *ms);
  * 0 tile Cholesky, 1 dense backward solve, 2 sigma0 mat-vec, 3 sparse forward
  * sweep, 4 sparse backward sweep (bench.py rooflines). */
 int32_t spb_ctx_bench_kernel(spb_ctx *ctx, int32_t which, int32_t reps, double *ms);
+/* Batch throughput (BASELINE config 5): n contexts (e.g. scenes sharing one
+ * factor) stepped concurrently, one stream each; mean device ms per round of
+ * one frame of every context. */
+int32_t spb_bench_batch(spb_ctx **ctxs, int32_t n, const spb_step_config *cfg, int32_t rounds,
+                        double *ms_per_round);
 
 /* ------------------------------------------------------- one-shot ops */
 int32_t spb_op_deformation_gradients(int64_t ne, const int64_t *tets, const double *dm_inverse, int64_t n,

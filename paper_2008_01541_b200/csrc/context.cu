@@ -125,9 +125,10 @@ struct Ctx {
   DBuf<int> k_ptr, k_idx;
   DBuf<double> k_val;
   // dense
-  int N = 0, ntasks = 0;
+  int N = 0, ntasks = 0, chol_grid = 0;
   DBuf<double> sigma0_tiles, L, LinvT, Y, gemv_partial, xrows;
   DBuf<int> flags, counter, info;
+  SweepWork sw;  // sparse-sweep workspace of this context
   DBuf<int2> tasks;
   DBuf<int> c22_tile_ptr, c22_ent_rc, c22_ent_ptr, c22_contrib;
   DenseDev dd{};
@@ -162,6 +163,7 @@ struct Ctx {
     if (cols_host) cudaFreeHost(cols_host);
     if (att_tgt_host) cudaFreeHost(att_tgt_host);
     if (io_host) cudaFreeHost(io_host);
+    sweep_work_free(sw);
     if (metrics_host) cudaFreeHost(metrics_host);
     if (st) cudaStreamDestroy(st);
   }
@@ -316,6 +318,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   if (n1 > 0) {
     TRY(build_device_factor(*f));
     TRY(U.zeros(3 * std::max<size_t>(device_factor_ubuf(*f->dev), 1)));
+    TRY(sweep_work_alloc(*f->dev, sw));
   }
   // beta gather (trailing-local keys) and proxies
   std::vector<int> key2(n, -1);
@@ -394,6 +397,10 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
     TRY(gemv_partial.zeros((size_t)nt * 6 * 64));
     std::vector<int2> tk = cholesky_task_order(N, true, CHOL_LEAD);
     ntasks = (int)tk.size();
+    // a column offers at most ~N parallel tiles: small problems leave SMs free
+    // for concurrent scenes (cfg5 batch); cfg3 uses every SM
+    chol_grid = std::max(1, std::min({NUM_SMS_B200, ntasks, std::max(8, 2 * N)}));
+    if (const char* e = getenv("SPB_CHOL_GRID")) chol_grid = std::max(8, std::min(ntasks, atoi(e)));
     TRY(tasks.upload(tk));
     // C22 entries: upper (c, r) COO contributions in (proxy, a, b) order, stored at
     // lower (r, c) (linalg.py:46-51, :67-74 + collision.py:431-434)
@@ -468,7 +475,7 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
     if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[1], st));
     // (3) forward substitution: y1 = L1^-1 f1[fill], f~2 = f2 - C y1
     if (n1 > 0) {
-      sparse_forward(st, *factor->dev, b.p, y.p, U.p, f_tilde2.p, &launches);
+      sparse_forward(st, *factor->dev, b.p, y.p, U.p, f_tilde2.p, &launches, &sw);
     } else if (n2 > 0) {
       SPB_CUDA(cudaMemcpyAsync(f_tilde2.p, b.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice, st));
     }
@@ -490,7 +497,7 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
       // (4.3)+(4.5) H = sigma0 + C22, LL^T = H, y = L^-1 g (one persistent launch), u2 = L^-T y
       SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
       SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
-      launch_cholesky_tiles(st, dd, tasks.p, ntasks, std::min(NUM_SMS_B200, ntasks));
+      launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid);
       launch_dense_backward(st, dd, xrows.p, u2.p);
       // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual
       launch_sym_tile_gemv(st, dd, u2.p, gemv_partial.p);
@@ -507,7 +514,7 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
       if (n2 > 0)
         SPB_CUDA(cudaMemcpyAsync(XF.p + 3 * (size_t)n1, u2acc.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice,
                                  st));
-      sparse_backward(st, *factor->dev, y.p, XF.p, &launches);
+      sparse_backward(st, *factor->dev, y.p, XF.p, &launches, &sw);
       launch_scatter_add(st, n1, x1_node.p, XF.p, x.p);
       launches++;
     }
@@ -845,7 +852,7 @@ int32_t spb_ctx_trace_cholesky(spb_ctx* cp, uint64_t* out, int32_t* tasks_out, i
   SPB_CUDA(cudaMemsetAsync(c->flags.p, (nd && nd[0] == '1') ? 2 : 0,
                            sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
   SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
-  spb::launch_cholesky_tiles(c->st, dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
+  spb::launch_cholesky_tiles(c->st, dd, c->tasks.p, c->ntasks, c->chol_grid);
   SPB_CUDA(cudaStreamSynchronize(c->st));
   SPB_CUDA(cudaMemcpy(out, tr, sizeof(unsigned long long) * 4 * c->ntasks, cudaMemcpyDeviceToHost));
   SPB_CUDA(cudaMemcpy(tasks_out, c->tasks.p, sizeof(int2) * c->ntasks, cudaMemcpyDeviceToHost));
@@ -871,15 +878,15 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
     case 0:
       cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st);
       cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st);
-      spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
+      spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid);
       break;
     case 1: spb::launch_dense_backward(c->st, c->dd, c->xrows.p, c->u2.p); break;
     case 2:
       spb::launch_sym_tile_gemv(c->st, c->dd, c->u2.p, c->gemv_partial.p);
       spb::launch_sym_tile_gemv_reduce(c->st, c->dd, c->gemv_partial.p, c->s0u.p);
       break;
-    case 3: spb::sparse_forward(c->st, *c->factor->dev, c->b.p, c->y.p, c->U.p, c->f_tilde2.p, nullptr); break;
-    case 4: spb::sparse_backward(c->st, *c->factor->dev, c->y.p, c->XF.p, nullptr); break;
+    case 3: spb::sparse_forward(c->st, *c->factor->dev, c->b.p, c->y.p, c->U.p, c->f_tilde2.p, nullptr, &c->sw); break;
+    case 4: spb::sparse_backward(c->st, *c->factor->dev, c->y.p, c->XF.p, nullptr, &c->sw); break;
   }
   cudaError_t ce = cudaStreamEndCapture(c->st, &g);
   if (ce != cudaSuccess) { spb::set_error(std::string("capture: ") + cudaGetErrorString(ce)); return SPB_ERR_CUDA; }
@@ -908,6 +915,41 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
   SPB_GUARD_END
 }
 
+// Aggregate device timing of several contexts stepped concurrently (one
+// stream each): `rounds` rounds, each one frame of every context; reports the
+// mean ms per round (the cfg5 batch: scenes sharing one factor on one GPU).
+int32_t spb_bench_batch(spb_ctx** ctxs, int32_t n, const spb_step_config* cfg, int32_t rounds, double* ms_per_round) {
+  SPB_GUARD_BEGIN
+  if (n <= 0 || !ctxs) { spb::set_error("no contexts"); return SPB_ERR_ARG; }
+  Ctx* c0 = reinterpret_cast<Ctx*>(ctxs[0]);
+  SPB_CUDA(cudaSetDevice(c0->device));
+  for (int k = 0; k < n; ++k) SPB_CUDA(cudaStreamSynchronize(reinterpret_cast<Ctx*>(ctxs[k])->st));
+  std::vector<cudaEvent_t> done(n);
+  cudaEvent_t e0, e1;
+  SPB_CUDA(cudaEventCreate(&e0));
+  SPB_CUDA(cudaEventCreate(&e1));
+  for (auto& e : done) SPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  SPB_CUDA(cudaEventRecord(e0, c0->st));
+  for (int k = 1; k < n; ++k) SPB_CUDA(cudaStreamWaitEvent(reinterpret_cast<Ctx*>(ctxs[k])->st, e0, 0));
+  for (int r = 0; r < rounds; ++r)
+    for (int k = 0; k < n; ++k) TRY(run_frame(reinterpret_cast<Ctx*>(ctxs[k]), cfg, nullptr));
+  for (int k = 1; k < n; ++k) {
+    Ctx* c = reinterpret_cast<Ctx*>(ctxs[k]);
+    SPB_CUDA(cudaEventRecord(done[k], c->st));
+    SPB_CUDA(cudaStreamWaitEvent(c0->st, done[k], 0));
+  }
+  SPB_CUDA(cudaEventRecord(e1, c0->st));
+  SPB_CUDA(cudaEventSynchronize(e1));
+  float ms;
+  SPB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_per_round = ms / std::max(rounds, 1);
+  for (auto& e : done) cudaEventDestroy(e);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
 int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);
@@ -925,7 +967,7 @@ int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
     SPB_CUDA(cudaMemsetAsync(c->flags.p, preset, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
     SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
     SPB_CUDA(cudaEventRecord(e0, c->st));
-    spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, std::min(spb::NUM_SMS_B200, c->ntasks));
+    spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid);
     SPB_CUDA(cudaEventRecord(e1, c->st));
     SPB_CUDA(cudaEventSynchronize(e1));
     float ms1;

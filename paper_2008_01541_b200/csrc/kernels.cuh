@@ -75,9 +75,19 @@ void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const doubl
 // ----------------------------------------------------------------- sparse.cu
 struct DeviceFactor;
 int build_device_factor(Factor& f);
+struct SweepWork {
+  double* VZ = nullptr;     // gathered rows (forward v / backward z)
+  double* P = nullptr;      // backward tile partials
+  int* chunk_cnt = nullptr; // backward chunk arrivals
+  int* flow_cnt = nullptr;  // dataflow counters
+};
+int sweep_work_alloc(const DeviceFactor& d, SweepWork& w);
+void sweep_work_free(SweepWork& w);
+// w == nullptr: the factor's own workspace (one-shot ops; not for concurrent use)
 void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
-                    int* launches);
-void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches);
+                    int* launches, const SweepWork* w = nullptr);
+void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches,
+                     const SweepWork* w = nullptr);
 size_t device_factor_ubuf(const DeviceFactor& df);
 int device_factor_levels(const DeviceFactor& df);
 

@@ -83,6 +83,7 @@ struct DeviceFactor {
   int* flow_cnt = nullptr;     // counters, zeroed per sweep: [claim | per supernode x 2 | per chunk]
   int fw_grid = 0, bw_grid = 0;
   size_t fw_smem = 0;
+  size_t p_slots = 0, nchunks = 0;  // sizes of the per-sweep workspace
   std::vector<LevelTasks> lv;
   std::vector<int> bwt_off, bwr_off, bww_off;  // backward tile / chunk / warp offsets per level
   ~DeviceFactor() {
@@ -1356,6 +1357,8 @@ int build_device_factor(Factor& f) {
     delete d;
     return rc;
   }
+  d->p_slots = std::max<size_t>(std::max(bwt.size(), flow_slots), 1);
+  d->nchunks = std::max<size_t>(bwr.size(), 1);
   if (cudaMalloc(&d->VZ, sizeof(double) * 3 * std::max<int64_t>(d->nrows_total, 1)) != cudaSuccess ||
       cudaMalloc(&d->P, sizeof(double) * 3 * BT_COLS * std::max<size_t>(std::max(bwt.size(), flow_slots), 1)) !=
           cudaSuccess) {
@@ -1383,19 +1386,40 @@ int build_device_factor(Factor& f) {
   return SPB_OK;
 }
 
+// Per-context sweep workspace (contexts sharing one factor step concurrently).
+int sweep_work_alloc(const DeviceFactor& d, SweepWork& w) {
+  w = SweepWork{};
+  if (cudaMalloc(&w.VZ, sizeof(double) * 3 * std::max<int64_t>(d.nrows_total, 1)) != cudaSuccess ||
+      cudaMalloc(&w.P, sizeof(double) * 3 * BT_COLS * d.p_slots) != cudaSuccess ||
+      cudaMalloc(&w.chunk_cnt, sizeof(int) * d.nchunks) != cudaSuccess ||
+      cudaMalloc(&w.flow_cnt, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch)) != cudaSuccess) {
+    sweep_work_free(w);
+    set_error("cudaMalloc failed (sweep workspace)");
+    return SPB_ERR_CUDA;
+  }
+  return SPB_OK;
+}
+void sweep_work_free(SweepWork& w) {
+  for (void* p : {(void*)w.VZ, (void*)w.P, (void*)w.chunk_cnt, (void*)w.flow_cnt})
+    if (p) cudaFree(p);
+  w = SweepWork{};
+}
+
 void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
-                    int* launches) {
+                    int* launches, const SweepWork* w) {
+  double* VZ = w ? w->VZ : d.VZ;
+  int* flow_cnt = w ? w->flow_cnt : d.flow_cnt;
   if (d.fuse > 0) {
     launch_pdl(k_subtree_forward, dim3(d.ngroups), dim3(SUB_THREADS), 0, st, (const SnDev*)d.sn, (const double*)d.M,
                (const int*)d.sub_pos, (const int*)d.sub_pos_off, (const int2*)d.sub_fw, (const int*)d.sub_fw_off,
-               d.fuse, (const int*)d.pos_owner, (const int*)d.asm_ptr, (const int*)d.asm_src, b, d.VZ, y, U);
+               d.fuse, (const int*)d.pos_owner, (const int*)d.asm_ptr, (const int*)d.asm_src, b, VZ, y, U);
     if (launches) ++*launches;
   }
   if (d.flow && d.nft > 0) {
-    cudaMemsetAsync(d.flow_cnt, 0, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch), st);
+    cudaMemsetAsync(flow_cnt, 0, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch), st);
     k_forward_flow<<<d.fw_grid, FL_FW_THREADS, d.fw_smem, st>>>(d.sn, d.M, d.ftasks, d.nft, d.f_need, d.parent,
-                                                                  d.flow_cnt, d.ns, d.pos_owner, d.asm_ptr, d.asm_src,
-                                                                  b, d.VZ, y, U);
+                                                                  flow_cnt, d.ns, d.pos_owner, d.asm_ptr, d.asm_src,
+                                                                  b, VZ, y, U);
     if (launches) ++*launches;
   }
   for (int l = d.fuse; l < d.nlevels && !d.flow; ++l) {
@@ -1403,12 +1427,12 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
     if (T.npos == 0) continue;
     launch_pdl(k_fw_gather, dim3(ceil_div(T.npos, 256)), dim3(256), 0, st, (const int*)(d.lvl_pos + T.pos_off),
                T.npos, (const int*)d.pos_owner, (const int*)d.asm_ptr, (const int*)d.asm_src, (const double*)U, b,
-               d.VZ);
+               VZ);
     const int grid = T.ncta + (T.nwarp + FW_WARPS - 1) / FW_WARPS;
     const size_t smem = sizeof(double) * std::max(3 * std::min(T.max_nc, CH_FW), 3 * FW_THREADS);
     launch_pdl(k_fw_level, dim3(grid), dim3(FW_THREADS), smem, st, (const SnDev*)d.sn, (const double*)d.M,
                (const int2*)(d.fw_cta + T.cta_off), T.ncta, (const int2*)(d.fw_warp + T.warp_off), T.nwarp,
-               T.rows, (const double*)d.VZ, y, U);
+               T.rows, (const double*)VZ, y, U);
     if (launches) *launches += 2;
   }
   if (d.n2 > 0) {
@@ -1418,16 +1442,21 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
   }
 }
 
-void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches) {
+void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, double* XF, int* launches,
+                     const SweepWork* w) {
+  double* VZ = w ? w->VZ : d.VZ;
+  double* Pw = w ? w->P : d.P;
+  int* chunk_cnt = w ? w->chunk_cnt : d.bw_chunk_cnt;
+  int* flow_cnt = w ? w->flow_cnt : d.flow_cnt;
   if (d.flow && d.nbt > 0) {
-    cudaMemsetAsync(d.flow_cnt, 0, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch), st);
+    cudaMemsetAsync(flow_cnt, 0, sizeof(int) * (1 + 2 * (size_t)d.ns + d.nbch), st);
     k_backward_flow<<<d.bw_grid, FL_BW_THREADS, 0, st>>>(d.sn, d.M, d.btasks, d.btask_chunk, d.nbt, d.bchunks,
-                                                                d.b_need, d.parent, d.flow_cnt, d.ns, d.pos_owner,
-                                                                d.rows, y, d.VZ, d.P, XF);
+                                                                d.b_need, d.parent, flow_cnt, d.ns, d.pos_owner,
+                                                                d.rows, y, VZ, Pw, XF);
     if (launches) ++*launches;
   }
   if (!d.flow && d.nlevels > d.fuse)
-    cudaMemsetAsync(d.bw_chunk_cnt, 0, sizeof(int) * std::max(d.bwr_off[d.nlevels], 1), st);
+    cudaMemsetAsync(chunk_cnt, 0, sizeof(int) * std::max(d.bwr_off[d.nlevels], 1), st);
   for (int l = d.nlevels - 1; l >= d.fuse && !d.flow; --l) {
     const LevelTasks& T = d.lv[l];
     if (T.npos == 0) continue;
@@ -1437,8 +1466,8 @@ void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, do
     if (nt)
       launch_pdl(k_bw_level, dim3(nt), dim3(256), sizeof(double) * 3 * T.bw_rows, st, (const SnDev*)d.sn,
                  (const double*)d.M, (const int4*)(d.bw_tiles + d.bwt_off[l]), T.bw_rows,
-                 (const int*)(d.bw_tile_chunk + d.bwt_off[l]), (const int4*)d.bw_chunks, d.bw_chunk_cnt,
-                 (const int*)d.pos_owner, (const int*)d.rows, y, d.P, XF);
+                 (const int*)(d.bw_tile_chunk + d.bwt_off[l]), (const int4*)d.bw_chunks, chunk_cnt,
+                 (const int*)d.pos_owner, (const int*)d.rows, y, Pw, XF);
     if (nw)
       launch_pdl(k_bw_level_warp, dim3((nw + 7) / 8), dim3(256), 0, st, (const SnDev*)d.sn, (const double*)d.M,
                  (const int*)(d.bw_warp + d.bww_off[l]), nw, (const int*)d.pos_owner, (const int*)d.rows, y, XF);
@@ -1447,7 +1476,7 @@ void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, do
   if (d.fuse > 0) {
     launch_pdl(k_subtree_backward, dim3(d.ngroups), dim3(SUB_THREADS), 0, st, (const SnDev*)d.sn,
                (const double*)d.M, (const int*)d.sub_pos, (const int*)d.sub_pos_off, (const int2*)d.sub_bw,
-               (const int*)d.sub_bw_off, d.fuse, (const int*)d.pos_owner, (const int*)d.rows, y, d.VZ, XF);
+               (const int*)d.sub_bw_off, d.fuse, (const int*)d.pos_owner, (const int*)d.rows, y, VZ, XF);
     if (launches) ++*launches;
   }
 }

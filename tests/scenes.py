@@ -36,14 +36,14 @@ def make_bar(cells=(6, 2, 2), extent=(1.5, 0.4, 0.4), press_depth=0.05, biphasic
     return model, system, state, part
 
 
-def block_yaml(cx, cy, cz, frac, h=0.05, frames=20, collider="plane", outer=1, inner=1):
+def block_yaml(cx, cy, cz, frac, h=0.05, frames=20, collider="plane", outer=1, inner=1, vel=-0.01):
     """SURVEY Appendix C block template (configs 2/3/5). collider 'plane' =
     half-space sinking 1 cm/frame; 'jaw' = capsule on a rotate motion
     (articulated self-contact emulation)."""
     ex, ey, ez = cx * h, cy * h, cz * h
     if collider == "plane":
         cold = (f"  - shape: {{half_space: {{point: [0.0, 0.0, {ez + 0.01}], normal: [0.0, 0.0, -1.0]}}}}\n"
-                f"    motion: {{kind: translate, velocity: [0.0, 0.0, -0.01]}}\n")
+                f"    motion: {{kind: translate, velocity: [0.0, 0.0, {vel}]}}\n")
     else:
         r = 0.3 * ey
         cold = (f"  - shape: {{capsule: {{p0: [{0.2 * ex}, -0.2, {ez + r - 0.02}], p1: [{0.2 * ex}, {ey + 0.2}, "
