@@ -205,6 +205,8 @@ int32_t spb_ctx_bench(spb_ctx *ctx, const spb_step_config *cfg, int32_t frames, 
 int32_t spb_ctx_trace_cholesky(spb_ctx *ctx, uint64_t *out, int32_t *tasks_out, int32_t *ntasks);
 /* Cholesky-only timing on the context's current H (tile kernel), ms per launch. */
 int32_t spb_ctx_bench_cholesky(spb_ctx *ctx, int32_t reps, double *ms);
+/* Diagnostics: per-block timestamps of one dense backward solve (5 per block). */
+int32_t spb_ctx_trace_dense_backward(spb_ctx *ctx, uint64_t *out, int32_t *nblocks);
 /* Graph-replay mean time of one piece of the frame on the current buffers:
  * 0 tile Cholesky, 1 dense backward solve, 2 sigma0 mat-vec, 3 sparse forward
  * sweep, 4 sparse backward sweep (bench.py rooflines). */

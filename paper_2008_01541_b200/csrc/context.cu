@@ -950,6 +950,25 @@ int32_t spb_bench_batch(spb_ctx** ctxs, int32_t n, const spb_step_config* cfg, i
   SPB_GUARD_END
 }
 
+// Diagnostics: per-CTA timestamps of one dense-backward launch (5 per block:
+// start, i>=j+3 sums done, c_j ready, x_{j+1} arrived, x_j stored).
+int32_t spb_ctx_trace_dense_backward(spb_ctx* cp, uint64_t* out, int32_t* nblocks) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  *nblocks = c->N;
+  if (!out || c->n2 == 0) return SPB_OK;
+  SPB_CUDA(cudaSetDevice(c->device));
+  unsigned long long* tr = nullptr;
+  SPB_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * 5 * c->N));
+  SPB_CUDA(cudaMemsetAsync(tr, 0, sizeof(unsigned long long) * 5 * c->N, c->st));
+  spb::launch_dense_backward(c->st, c->dd, c->xrows.p, c->u2.p, tr);
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  SPB_CUDA(cudaMemcpy(out, tr, sizeof(unsigned long long) * 5 * c->N, cudaMemcpyDeviceToHost));
+  cudaFree(tr);
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
 int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);

@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
 // step costs one store -> load visibility instead of store, fence, release
 // flag, poll, acquire and reload.
 constexpr int BW_LDS = 65;  // padded row stride of the shared tiles (conflict-free column access)
-constexpr int BW_SMEM_DOUBLES = 4 * TS * BW_LDS + 6 * TS + 12 * TS + 3 * TS + 1;
+constexpr int BW_SMEM_DOUBLES = 4 * TS * BW_LDS + 6 * TS + 12 * TS + 3 * TS + 3 * TS + 1;
 constexpr unsigned long long BW_EMPTY = ~0ull;  // sentinel (negative NaN, all payload bits set)
 
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const double* p) {
@@ -720,7 +720,10 @@ __device__ __forceinline__ double bw_reduce(const double* part, int tid) {
 }
 
 __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __restrict__ xrows /* N*3*64 */,
-                                                        double* __restrict__ u, int m) {
+                                                        double* __restrict__ u, int m,
+                                                        unsigned long long* __restrict__ trace /* 5 per CTA or null */) {
+  unsigned long long tt[5] = {0, 0, 0, 0, 0};
+  if (trace && threadIdx.x == 0) tt[0] = globaltimer();
   extern __shared__ double bw_sm[];
   double* sW = bw_sm;                   // W[k][c] = inv(L_jj)[c][k]
   double* sM = sW + TS * BW_LDS;        // M = L_{j+1,j} W
@@ -729,7 +732,9 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
   double* xi = sL2 + TS * BW_LDS;       // 2 x 3 x 64
   double* part = xi + 6 * TS;           // 4 x 3 x 64 partial sums
   double* cj = part + 12 * TS;          // 3 x 64
-  int* nflag = reinterpret_cast<int*>(cj + 3 * TS);
+  double* yj = cj + 3 * TS;             // 3 x 64: y_j, prefetched
+  int* nflag = reinterpret_cast<int*>(yj + 3 * TS);
+  double* sM2 = sL1;                    // M2 = L_{j+2,j} W (overwrites L_{j+1,j} once M is formed)
   const int N = d.N;
   const int j = N - 1 - blockIdx.x;
   const int tid = threadIdx.x;
@@ -741,17 +746,24 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
     if (j + 1 < N) sL1[k * BW_LDS + cc] = d.L[(size_t)tidx(j + 1, j) * TILE + swz(k, cc)];
     if (j + 2 < N) sL2[k * BW_LDS + cc] = d.L[(size_t)tidx(j + 2, j) * TILE + swz(k, cc)];
   }
+  if (tid < 3 * TS) yj[tid] = d.Y[(size_t)j * TILE + swz(tid >> 6, c)];
   __syncthreads();
-  if (j + 1 < N) {
-    // M[k][c] = sum_p L1[k][p] W[p][c]: thread (grp, c) forms rows k = grp + 4 q
+  // M[k][c] = sum_p A[k][p] W[p][c] for A = L_{j+1,j} and (then) L_{j+2,j}:
+  // thread (grp, c) forms rows k = grp + 4 q
+  auto times_w = [&](const double* A, double* out) {
 #pragma unroll 1
     for (int q = 0; q < 16; ++q) {
       const int k = grp + 4 * q;
       double s = 0.0;
 #pragma unroll 16
-      for (int p = 0; p < TS; ++p) s = fma(sL1[k * BW_LDS + p], sW[p * BW_LDS + c], s);
-      sM[k * BW_LDS + c] = s;
+      for (int p = 0; p < TS; ++p) s = fma(A[k * BW_LDS + p], sW[p * BW_LDS + c], s);
+      out[k * BW_LDS + c] = s;
     }
+  };
+  if (j + 1 < N) times_w(sL1, sM);
+  if (j + 2 < N) {
+    __syncthreads();  // L_{j+1,j} consumed: its buffer takes M2
+    times_w(sL2, sM2);
   }
   // ---- contributions of x_i, i >= j+3, from the global tiles: the next two
   // tiles are loaded into registers ahead of their x, and when this CTA is
@@ -792,31 +804,32 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
       __syncthreads();
     }
   }
-  // ---- x_{j+2} from the prefetched tile, then c_j = (y_j - acc) W
-  if (j + 2 < N) {
-    bw_fetch(xrows, j + 2, xi, -1, nflag);
-#pragma unroll
-    for (int k = grp * 16; k < grp * 16 + 16; ++k) {
-      const double l = sL2[k * BW_LDS + c];
-      acc0 += xi[k] * l;
-      acc1 += xi[TS + k] * l;
-      acc2 += xi[2 * TS + k] * l;
-    }
-  }
+  if (trace && threadIdx.x == 0) tt[1] = globaltimer();
+  // ---- c'_j = (y_j - sum_{i>=j+3} x_i L_ij) W as soon as those sums are in;
+  // then x_{j+2} costs one GEMV with M2 = L_{j+2,j} W when it arrives
   part[(grp * 3 + 0) * TS + c] = acc0;
   part[(grp * 3 + 1) * TS + c] = acc1;
   part[(grp * 3 + 2) * TS + c] = acc2;
   __syncthreads();
-  if (tid < 3 * TS) xi[tid] = d.Y[(size_t)j * TILE + swz(tid >> 6, c)] - bw_reduce(part, tid);
+  if (tid < 3 * TS) xi[tid] = yj[tid] - bw_reduce(part, tid);
   __syncthreads();
   bw_gemv_part(xi, sW, part, c, grp);
   __syncthreads();
   if (tid < 3 * TS) cj[tid] = bw_reduce(part, tid);
+  if (j + 2 < N) {
+    __syncthreads();  // xi and part free
+    bw_fetch(xrows, j + 2, xi, -1, nflag);
+    bw_gemv_part(xi, sM2, part, c, grp);
+    __syncthreads();
+    if (tid < 3 * TS) cj[tid] -= bw_reduce(part, tid);
+  }
+  if (trace && threadIdx.x == 0) tt[2] = globaltimer();
   // ---- the chain step: x_j = c_j - x_{j+1} M
   double x = 0.0;
   if (j + 1 < N) {
     __syncthreads();  // cj complete; xi free
     bw_fetch(xrows, j + 1, xi, -1, nflag);
+    if (trace && threadIdx.x == 0) tt[3] = globaltimer();
     bw_gemv_part(xi, sM, part, c, grp);
     __syncthreads();
     if (tid < 3 * TS) x = cj[tid] - bw_reduce(part, tid);
@@ -826,6 +839,10 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
   if (tid < 3 * TS) {
     if (isnan(x)) x = CUDART_NAN;  // canonical: never the sentinel
     st_relaxed_f64(xrows + (size_t)j * 3 * TS + tid, x);
+    if (trace && threadIdx.x == 0) {
+      tt[4] = globaltimer();
+      for (int k = 0; k < 5; ++k) trace[5 * (size_t)blockIdx.x + k] = tt[k];
+    }
     const int row = j * TS + c;
     if (row < m) u[3 * row + (tid >> 6)] = x;
   }
@@ -945,7 +962,8 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
   k_cholesky_tiles<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
 }
 
-void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u) {
+void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u,
+                           unsigned long long* trace) {
   static bool attr = false;
   const size_t smem = sizeof(double) * BW_SMEM_DOUBLES;
   if (!attr) {
@@ -953,7 +971,7 @@ void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, do
     attr = true;
   }
   cudaMemsetAsync(xrows, 0xff, sizeof(double) * 3 * TS * (size_t)d.N, st);  // BW_EMPTY everywhere
-  k_dense_backward<<<d.N, 256, smem, st>>>(d, xrows, u, d.m);
+  k_dense_backward<<<d.N, 256, smem, st>>>(d, xrows, u, d.m, trace);
 }
 
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial) {

@@ -68,7 +68,8 @@ size_t cholesky_smem_bytes();
 void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid);
 std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead);
 constexpr int CHOL_LEAD = 2;
-void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u);
+void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u,
+                           unsigned long long* trace = nullptr);
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial);
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out);
 
