@@ -285,9 +285,14 @@ __device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j
       // next pivot is one shuffle away
       dnext = shfl_f64(fma(-lm, l, v[k + 1]), k + 1);
     }
+    // broadcast the column through shared memory: one store per lane and one
+    // broadcast load per entry instead of two 32-bit shuffles per entry
+    double* lb = DT + 16 * LDT + 16 * (k & 1);
+    if (lane < 16) lb[lane] = l;
+    __syncwarp();
 #pragma unroll 16
     for (int c = 0; c < 16; ++c) {
-      if (c > k) v[c] = fma(-lm, shfl_f64(l, c), v[c]);
+      if (c > k) v[c] = fma(-lm, lb[c], v[c]);
     }
   }
   if (badk >= 0 && lane == 0) atomicCAS(info, 0, j * TS + o + badk + 1);
