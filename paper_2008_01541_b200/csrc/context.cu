@@ -142,6 +142,8 @@ struct Ctx {
   double* att_tgt_host = nullptr;    // pinned staging
   char* io_host = nullptr;           // pinned staging for set_state / get_state
   size_t io_bytes = 0;
+  cudaStream_t st_io = nullptr;      // state download overlapping the metrics kernels
+  cudaEvent_t ev_state = nullptr;    // recorded between the solve and the metrics: the state is final
   // metrics
   DBuf<double> e_part, a_part, p_part, r_part, metrics_out;
   double* metrics_host = nullptr;    // pinned
@@ -151,25 +153,32 @@ struct Ctx {
   DBuf<double> Gall, fall;
   DBuf<int> gall_ptr, gall_src, att_ptr_node, att_idx_node, node_ids;
   // graph cache
-  std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>> graphs;  // solve, metrics
   int last_launches = 0;
   bool residual_valid = false;
 
   ProxyDev px() const { return ProxyDev{P, prox_elem.p, prox_w.p, prox_c.p, prox_local.p}; }
 
   ~Ctx() {
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : graphs) {
+      cudaGraphExecDestroy(kv.second.first);
+      cudaGraphExecDestroy(kv.second.second);
+    }
     for (double* v : shape_vals) cudaFree(v);
     if (cols_host) cudaFreeHost(cols_host);
     if (att_tgt_host) cudaFreeHost(att_tgt_host);
     if (io_host) cudaFreeHost(io_host);
     sweep_work_free(sw);
     if (metrics_host) cudaFreeHost(metrics_host);
+    if (ev_state) cudaEventDestroy(ev_state);
+    if (st_io) cudaStreamDestroy(st_io);
     if (st) cudaStreamDestroy(st);
   }
 
   int create(const spb_scene_desc* s, Factor* f, int dev);
-  int enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev /* 7 phase events or null */);
+  // one frame = solve (outer/inner passes, state final) + metrics
+  int enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev /* 6 phase events or null */);
+  int enqueue_metrics(cudaEvent_t* ev);
   int sync_shapes();
   int io_reserve(size_t bytes) {
     if (bytes <= io_bytes) return SPB_OK;
@@ -225,20 +234,23 @@ static int io_upload(Ctx* c, const IoList& l, bool sync = true) {
   return SPB_OK;
 }
 
-static int io_download(Ctx* c, const IoList& l) {
+static int io_download(Ctx* c, const IoList& l, cudaStream_t st = nullptr, bool wait_state = false) {
+  if (!st) st = c->st;
   TRY(c->io_reserve(l.total));
+  if (wait_state) SPB_CUDA(cudaStreamWaitEvent(st, c->ev_state, 0));
   size_t off = 0;
   bool staged[8] = {};
   for (int i = 0; i < l.n; ++i) {
     if (host_pinned(l.items[i].host)) {
-      SPB_CUDA(cudaMemcpyAsync(l.items[i].host, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, c->st));
+      SPB_CUDA(cudaMemcpyAsync(l.items[i].host, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, st));
       continue;
     }
     staged[i] = true;
-    SPB_CUDA(cudaMemcpyAsync(c->io_host + off, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, c->st));
+    SPB_CUDA(cudaMemcpyAsync(c->io_host + off, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, st));
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
-  SPB_CUDA(cudaStreamSynchronize(c->st));
+  SPB_CUDA(cudaStreamSynchronize(st));
+  if (st != c->st) SPB_CUDA(cudaStreamSynchronize(c->st));
   off = 0;
   for (int i = 0; i < l.n; ++i) {
     if (!staged[i]) continue;
@@ -252,6 +264,8 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   device = dev;
   SPB_CUDA(cudaSetDevice(device));
   SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  SPB_CUDA(cudaStreamCreateWithFlags(&st_io, cudaStreamNonBlocking));
+  SPB_CUDA(cudaEventCreateWithFlags(&ev_state, cudaEventDisableTiming));
   factor = f;
   n = s->num_nodes;
   ne = s->num_elements;
@@ -460,7 +474,7 @@ int Ctx::sync_shapes() {
 // ev (optional): 7 events recorded at phase boundaries of the LAST pass:
 //   0 start, 1 after local+forces, 2 after forward, 3 after inner loop,
 //   4 after backward, 5 after metrics.
-int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
+int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
   int launches = 0;
   const ProxyDev P_ = px();
   bool first_detection_done = false;
@@ -520,7 +534,14 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
     }
     if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[4], st));
   }
-  // metrics: full-mesh energy, max penetration, active count, residual
+  last_launches = launches;
+  return SPB_OK;
+}
+
+// metrics: full-mesh energy, max penetration, active count, residual
+int Ctx::enqueue_metrics(cudaEvent_t* ev) {
+  const ProxyDev P_ = px();
+  int launches = 0;
   launch_elastic_energy(st, ne, tets.p, x.p, dmi.p, vol.p, R.p, Q.p, ep, e_part.p);
   launch_attachment_energy(st, na, att_nodes.p, att_k.p, att_tgt.p, x.p, a_part.p);
   launch_proxy_final(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, p_part.p);
@@ -528,7 +549,7 @@ int Ctx::enqueue_frame(int outer, int inner, int cadence, cudaEvent_t* ev) {
                         residual_valid ? r_blocks : 0, active.p, P, 1, metrics_out.p);
   launches += 4;
   if (ev) SPB_CUDA(cudaEventRecord(ev[5], st));
-  last_launches = launches;
+  last_launches += launches;
   return SPB_OK;
 }
 
@@ -694,6 +715,9 @@ int32_t spb_ctx_get_state(spb_ctx* cp, double* x, double* R, double* Q, uint8_t*
   SPB_GUARD_END
 }
 
+// One frame on the context stream. Between the solve and the metrics the
+// host records ev_state (the state is final), so a download on the io stream
+// can overlap the metrics kernels with plain stream-order semantics.
 static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
   const int outer = cfg->outer_iters, inner = cfg->inner_iters, cad = cfg->cadence;
   TRY(c->sync_shapes());
@@ -701,21 +725,27 @@ static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
     auto key = std::make_tuple(outer, inner, cad);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
-      cudaGraph_t gph;
-      SPB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
-      int rc = c->enqueue_frame(outer, inner, cad, nullptr);
-      cudaError_t e2 = cudaStreamEndCapture(c->st, &gph);
-      if (rc != SPB_OK) return rc;
-      if (e2 != cudaSuccess) { spb::set_error(std::string("graph capture: ") + cudaGetErrorString(e2)); return SPB_ERR_CUDA; }
-      cudaGraphExec_t exe;
-      SPB_CUDA(cudaGraphInstantiate(&exe, gph, 0));
-      cudaGraphDestroy(gph);
-      it = c->graphs.emplace(key, exe).first;
+      cudaGraphExec_t exe[2];
+      for (int part = 0; part < 2; ++part) {
+        cudaGraph_t gph;
+        SPB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+        int rc = part == 0 ? c->enqueue_solve(outer, inner, cad, nullptr) : c->enqueue_metrics(nullptr);
+        cudaError_t e2 = cudaStreamEndCapture(c->st, &gph);
+        if (rc != SPB_OK) return rc;
+        if (e2 != cudaSuccess) { spb::set_error(std::string("graph capture: ") + cudaGetErrorString(e2)); return SPB_ERR_CUDA; }
+        SPB_CUDA(cudaGraphInstantiate(&exe[part], gph, 0));
+        cudaGraphDestroy(gph);
+      }
+      it = c->graphs.emplace(key, std::make_pair(exe[0], exe[1])).first;
     }
-    SPB_CUDA(cudaGraphLaunch(it->second, c->st));
+    SPB_CUDA(cudaGraphLaunch(it->second.first, c->st));
+    SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
+    SPB_CUDA(cudaGraphLaunch(it->second.second, c->st));
     return SPB_OK;
   }
-  return c->enqueue_frame(outer, inner, cad, ev);
+  TRY(c->enqueue_solve(outer, inner, cad, ev));
+  SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
+  return c->enqueue_metrics(ev);
 }
 
 // Enqueue one frame and the metrics read-back; no synchronisation.
@@ -793,9 +823,10 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
   if (c->P) down.add(c->target.p, target, sizeof(double) * 3 * c->P);
   if (c->n2) down.add(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2);
   if (c->n2) down.add(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2);
-  // the staging area is shared by the upload and the download: the download
-  // lands behind the upload's copies in stream order, so one sync covers both
-  TRY(io_download(c, down));
+  // the download runs on the io stream from the in-graph "state final" event
+  // (behind the upload's copies, which precede the graph on the main stream),
+  // overlapping the metrics kernels; both streams are synchronised
+  TRY(io_download(c, down, c->st_io, true));
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return frame_finish(c, m);
   SPB_GUARD_END
@@ -820,7 +851,8 @@ int32_t spb_ctx_bench(spb_ctx* cp, const spb_step_config* cfg, int32_t frames, d
   if (phase_ms) {
     cudaEvent_t ev[6];
     for (auto& e : ev) SPB_CUDA(cudaEventCreate(&e));
-    TRY(c->enqueue_frame(cfg->outer_iters, cfg->inner_iters, cfg->cadence, ev));
+    TRY(c->enqueue_solve(cfg->outer_iters, cfg->inner_iters, cfg->cadence, ev));
+    TRY(c->enqueue_metrics(ev));
     SPB_CUDA(cudaStreamSynchronize(c->st));
     for (int k = 0; k < 5; ++k) {
       float a = 0;
