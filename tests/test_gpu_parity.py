@@ -275,3 +275,29 @@ def test_inner_keeps_x1_frozen_and_rhs_maintenance():
     _, scratch = P.forward_sub(system.factor, f[system.x1_ids], f[system.x2_ids])
     scale = max(np.abs(scratch).max(), np.abs(state.f_tilde2).max())
     assert np.abs(state.f_tilde2 - scratch).max() < 1e-9 * scale
+
+
+@pytest.mark.parametrize("env", [{"SPB_SWEEP_FLOW": "1"}, {"SPB_SWEEP_FUSE": "0"}, {"SPB_SWEEP_FUSE": "99"}])
+def test_sweep_variants_match(monkeypatch, env):
+    """The sweep schedules (dataflow kernels, no fused subtrees, everything in
+    subtrees) are alternative orders of the same per-supernode arithmetic:
+    each must agree with the default level schedule to roundoff."""
+    from scenes import block_yaml
+
+    def sweep(extra):
+        for k, v in extra.items():
+            monkeypatch.setenv(k, v)
+        sim = P.Simulation(P.parse_scenario(block_yaml(16, 10, 8, 0.75)), diagnostics=False)
+        f = sim.system.factor
+        rng = np.random.default_rng(7)
+        b1 = rng.normal(size=(f.n1, 3)); b2 = rng.normal(size=(f.n2, 3)); x2 = rng.normal(size=(f.n2, 3))
+        y1, y2 = P.forward_sub(f, b1, b2)
+        x1 = P.backward_sub(f, y1, x2)
+        for k in extra:
+            monkeypatch.delenv(k)
+        return y1, y2, x1
+
+    ref = sweep({})
+    alt = sweep(env)
+    for a, b in zip(ref, alt):
+        assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
