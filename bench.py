@@ -430,6 +430,151 @@ def run_batch(args):
         dist.destroy_process_group()
 
 
+CFG4_SIZES = (2048, 4096, 6144, 8192, 12288, 16384, 24576, 49152)
+
+
+def run_dense(args):
+    """BASELINE config 4: the dense Schur-complement Cholesky sweep.
+
+    Orders 2K-49K (SURVEY.md §8d reads "6K-48K DOFs" both as dense orders
+    6,144-49,152 and, counted like config 3's 3m, as 2,048-16,384), FP64,
+    synthetic SPD matrices generated on the device (exponential kernel on a
+    surface grid, kappa ~1e2). One GPU: the persistent tile kernel. N GPUs
+    (torchrun): the tile-cyclic factorization, tiles pushed into the peers'
+    replicas over NVLink; time = max over ranks, scaling "strong" (one matrix
+    per size, whatever N). `value` = TFLOP/s (m^3/3 per factorization) at the
+    largest order; every order is checked by ||A v - L L^T v|| / ||A v||."""
+    import torch
+
+    from paper_2008_01541_b200 import dense as D
+
+    rank, world, local = _env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+
+        torch.cuda.set_device(local)
+        dist_mod.init_process_group("nccl")
+        dist = dist_mod
+    sizes = [int(v) for v in args.sizes.split(",")] if args.sizes else list(CFG4_SIZES)
+    clk = ClockSampler(local)
+    clk.__enter__()
+    sweep = []
+    launches = 0
+    for m in sizes:
+        if world > 1:
+            tc = D.TileCyclicCholesky(m, device=local)
+            dc = tc.dense
+            run = tc.factor
+        else:
+            dc = D.DenseCholesky(m, device=0)
+            run = lambda: dc.factor(1)  # noqa: E731
+        dc.synthetic()
+        est_ms = D.chol_flops(m) / 30e12 * 1e3 / world
+        steps = max(2, min(args.steps, int(4000.0 / max(est_ms, 1e-3))))
+        for _ in range(args.warmup):
+            run()
+        times = [run() for _ in range(steps)]
+        launches += steps
+        ms = max_over_ranks(dist, float(np.mean(times)))
+        rr, aa = dc.residual(np.random.default_rng(m).standard_normal(m))
+        sweep.append({"m": m, "ms": ms, "tflops": D.chol_flops(m) / (ms * 1e-3) / 1e12, "steps": steps,
+                      "rel_residual": rr / aa, "tiles": (m + 63) // 64})
+        del dc
+        if world > 1:
+            del tc
+        torch.cuda.empty_cache()
+    clk.__exit__(None, None, None)
+    # e2e through the C ABI with host buffers: upload A, factor, download L
+    # (largest order whose two host copies stay within a few GB)
+    e2e = None
+    if world == 1:
+        me = max(m for m in sizes if m <= 16384) if any(m <= 16384 for m in sizes) else min(sizes)
+        a = np.zeros((me, me))
+        dc = D.DenseCholesky(me, device=0)
+        dc.synthetic()
+        a[:] = dc.matrix()
+        reps = 3
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            dc.set_matrix(a)
+            dc.factor(1)
+            L = dc.factor_lower()
+        e2e_s = (time.perf_counter() - t0) / reps
+        launches += reps
+        e2e = {"value": D.chol_flops(me) / e2e_s / 1e12, "unit": "TFLOP/s", "m": me,
+               "h2d_bytes_per_step": 8 * me * me, "d2h_bytes_per_step": 8 * me * me}
+        del dc, L
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    fp64_peak = measure_fp64_peak()
+    top = sweep[-1]
+    line = {
+        "metric": "Cholesky FP64 TFLOPS (dense Schur-complement sweep, BASELINE config 4)",
+        "value": top["tflops"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": top["ms"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic SPD (exponential kernel on a surface grid, generated on the device)",
+        "config": {"workload": f"cfg4: dense SPD order {top['m']} (sweep {sizes[0]}-{sizes[-1]})",
+                   "sizes": sizes, "l2": "L and A tiles of every order >= 6144 exceed the 126 MB L2",
+                   "parallelism": ("tile-cyclic over %d GPUs (NVLink peer pushes)" % world) if world > 1
+                   else "one GPU"},
+        "sweep": sweep,
+        "roofline": {"bound": "tensor", "kernel": "k_cholesky_tiles (FP64 DMMA)" if world == 1 else
+                     "k_cholesky_ranks (FP64 DMMA, tile-cyclic)", "achieved": top["tflops"] / world,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": top["tflops"] / world / fp64_peak,
+                     "traffic": None, "flops_per_launch": D.chol_flops(top["m"]),
+                     "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (per GPU)"},
+        "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_dpotrf(args.cpu_m)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def cpu_dpotrf(m: int):
+    """The reference's own dense factor path on host cores: scipy.linalg.cholesky
+    (LAPACK dpotrf, linalg.py:437) on a bounded sample order m."""
+    import scipy.linalg as sla
+
+    threads = os.cpu_count() or 1
+    g = int(np.ceil(np.sqrt(m)))
+    r = np.arange(m)
+    p = np.stack([r % g, r // g], 1).astype(float)
+    dd = np.sqrt(((p[:, None, :] - p[None, :, :]) ** 2).sum(-1))
+    a = 4950.0 * np.exp(-dd / 2.0) + 50.0 * np.eye(m)
+    sla.cholesky(a, lower=True)
+    t = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        sla.cholesky(a, lower=True)
+        t.append(time.perf_counter() - t0)
+    sec = float(np.median(t))
+    return {"value": m ** 3 / 3.0 / sec / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+            "sample": f"scipy.linalg.cholesky (LAPACK dpotrf, the reference's linalg.py:437 call) at order {m}, "
+                      f"median of 3: {1e3 * sec:.1f} ms"}
+
+
+def run_dense_reference(args):
+    rank, _, _ = _env_rank()
+    if rank != 0:
+        return
+    m = args.cpu_m
+    cb = cpu_dpotrf(m)
+    print(json.dumps({
+        "impl": "reference", "metric": "Cholesky FP64 TFLOPS (dense Schur-complement sweep, BASELINE config 4)",
+        "value": cb["value"], "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": 3, "warmup": 1,
+        "ms_per_step": m ** 3 / 3.0 / (cb["value"] * 1e12) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic SPD",
+        "config": {"workload": f"cfg4: dense SPD order {m} (bounded CPU sample)"},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+        flush=True)
+
+
 def met_launches(ds, cfg):
     import ctypes
 
@@ -447,18 +592,24 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg5"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--outer", type=int, default=1)
     ap.add_argument("--inner", type=int, default=1)
     ap.add_argument("--cpu-frames", type=int, default=3)
     ap.add_argument("--ref-frames", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scenes", type=int, default=1, help="batch mode: concurrent scenes per GPU (cfg5)")
+    ap.add_argument("--sizes", default="", help="cfg4: comma-separated dense orders (default 2048..49152)")
+    ap.add_argument("--cpu-m", type=int, default=6144, help="cfg4: order of the CPU dpotrf sample")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.impl == "reference" and args.config == "cfg4":
+        run_dense_reference(args)
+    elif args.impl == "reference":
         run_reference(args)
+    elif args.config == "cfg4":
+        run_dense(args)
     elif args.scenes > 1:
         run_batch(args)
     else:

@@ -24,6 +24,9 @@
  *                          collision.detect/penetration_depths (collision.py:316-359)
  *                          linalg.forward_sub/backward_sub  (linalg.py:385-414)
  *                          linalg.dense_factor/dense_solve  (linalg.py:432-461)
+ *   spb_dense_*         <- linalg.dense_factor as a standalone, possibly
+ *                          tile-cyclic multi-GPU factorization (linalg.py:432-440;
+ *                          BASELINE config 4)
  *
  * Conventions: plain pointers and sizes, no torch types. All arrays are
  * host memory, C-contiguous, float64 / int64 unless stated. Every call returns
@@ -237,6 +240,43 @@ int32_t spb_op_dense_solve(int64_t m, const double *chol, int64_t nrhs, const do
 int32_t spb_op_forward_sub(const spb_factor *f, int64_t nrhs, const double *b1, const double *b2, double *y1,
                            double *y2);
 int32_t spb_op_backward_sub(const spb_factor *f, int64_t nrhs, const double *y1, const double *x2, double *x1);
+
+/* ------------------------------------- standalone dense Cholesky (config 4)
+ * Replaces linalg.dense_factor (linalg.py:432-440: scipy.linalg.cholesky,
+ * LAPACK dpotrf, lower) for one m x m SPD matrix held on the device as 64x64
+ * tiles, factored by the frame solver's persistent tile kernel.
+ * nranks == 1: one GPU. nranks > 1, emulate == 0: tile-cyclic over nranks
+ * processes (one per GPU, `rank` = this process): each rank keeps a full L
+ * replica and pushes every tile it finishes into the peers' replicas over
+ * NVLink (CUDA IPC); exchange handles with spb_dense_ipc_handle /
+ * spb_dense_open_peers, then per factorization on every rank:
+ *   spb_dense_reset -> barrier -> spb_dense_launch -> spb_dense_finish -> barrier
+ * emulate == 1: all nranks replicas on this one GPU, factored by ONE launch
+ * (tests of the multi-rank data path on a single GPU). info: dpotrf's first
+ * failing column (1-based), SPB_ERR_INDEFINITE when > 0. */
+typedef struct spb_dense spb_dense;
+#define SPB_DENSE_IPC_BYTES 64
+int32_t spb_dense_create(int64_t m, int32_t device, int32_t rank, int32_t nranks, int32_t emulate,
+                         spb_dense **out);
+void spb_dense_destroy(spb_dense *d);
+/* the lower triangle of a row-major m x m matrix is read (then mirrored) */
+int32_t spb_dense_set_matrix(spb_dense *d, const double *h);
+/* K_rc = a exp(-|p_r - p_c| / ell) + b delta_rc on a ceil(sqrt(m))^2 grid, generated on the device */
+int32_t spb_dense_synthetic(spb_dense *d, double a, double b, double ell);
+int32_t spb_dense_get_matrix(spb_dense *d, double *h /* m x m row-major, symmetric */);
+int32_t spb_dense_get_factor(spb_dense *d, int32_t replica, double *chol /* m x m row-major, lower */);
+int32_t spb_dense_ipc_handle(spb_dense *d, uint8_t *out /* SPB_DENSE_IPC_BYTES */);
+int32_t spb_dense_open_peers(spb_dense *d, const uint8_t *handles /* nranks * SPB_DENSE_IPC_BYTES, rank order */);
+int32_t spb_dense_reset(spb_dense *d);
+int32_t spb_dense_launch(spb_dense *d);
+int32_t spb_dense_finish(spb_dense *d, double *ms, int64_t *info);
+/* single-process convenience: reps x (reset, launch, finish); mean ms per factorization */
+int32_t spb_dense_factor(spb_dense *d, int32_t reps, double *ms, int64_t *info);
+/* out2 = { ||A v - L (L^T v)||_2, ||A v||_2 } on the device (full-size check) */
+int32_t spb_dense_residual(spb_dense *d, int32_t replica, const double *v, double *out2);
+/* host only: the (i, j) tile tasks rank `rank` of nranks runs, in claim order;
+ * ij == NULL returns the count; else *count is the capacity (pairs) */
+int32_t spb_dense_rank_tasks(int64_t m, int32_t rank, int32_t nranks, int32_t *ij, int64_t *count);
 
 #ifdef __cplusplus
 }

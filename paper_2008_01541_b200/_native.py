@@ -110,6 +110,20 @@ _SIGS = {
     "spb_op_dense_solve": ([I64, P, I64, P, P], I32),
     "spb_op_forward_sub": ([P, I64, P, P, P, P], I32),
     "spb_op_backward_sub": ([P, I64, P, P, P], I32),
+    "spb_dense_create": ([I64, I32, I32, I32, I32, P], I32),
+    "spb_dense_destroy": ([P], None),
+    "spb_dense_set_matrix": ([P, P], I32),
+    "spb_dense_synthetic": ([P, F64, F64, F64], I32),
+    "spb_dense_get_matrix": ([P, P], I32),
+    "spb_dense_get_factor": ([P, I32, P], I32),
+    "spb_dense_ipc_handle": ([P, P], I32),
+    "spb_dense_open_peers": ([P, P], I32),
+    "spb_dense_reset": ([P], I32),
+    "spb_dense_launch": ([P], I32),
+    "spb_dense_finish": ([P, P, P], I32),
+    "spb_dense_factor": ([P, I32, P, P], I32),
+    "spb_dense_residual": ([P, I32, P, P], I32),
+    "spb_dense_rank_tasks": ([I64, I32, I32, P, P], I32),
 }
 EXPORTED = tuple(_SIGS)
 

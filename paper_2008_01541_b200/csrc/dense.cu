@@ -97,12 +97,33 @@ __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"
 
 // Spin (one thread) until a readiness flag is set, then order later reads
 // (generic and async proxy) after the producer's release.
+// MULTI: the flag may be released by a peer GPU (system scope).
+template <bool MULTI = false>
 __device__ __forceinline__ void poll_flag(const int* f, int v) {
-  if (ld_relaxed(f) < v) {
-    while (ld_relaxed(f) < v) __nanosleep(32);
+  if (MULTI) {
+    if (ld_relaxed_sys(f) < v) {
+      while (ld_relaxed_sys(f) < v) __nanosleep(64);
+    }
+    fence_acq_rel_sys();
+  } else {
+    if (ld_relaxed(f) < v) {
+      while (ld_relaxed(f) < v) __nanosleep(32);
+    }
+    fence_acq_rel_gpu();
   }
-  fence_acq_rel_gpu();
   fence_proxy_async_global();
+}
+
+// Tile-cyclic mode: after a CTA's threads stored a finished tile into the
+// local and the peer replicas, order those stores before the flag releases.
+template <bool MULTI>
+__device__ __forceinline__ void fence_tile_stores() {
+  if (MULTI) __threadfence_system();
+  else __threadfence();
+}
+// thread 0: release flag `idx` with value v in every peer replica
+__device__ __forceinline__ void release_peers(const DensePeers& pr, int idx, int v) {
+  for (int p = 0; p < pr.n; ++p) st_release_sys(pr.flags[p] + idx, v);
 }
 
 // Warp tile 32 rows x 16 cols; 8 warps cover 64x64 as 2 x 4.
@@ -345,8 +366,9 @@ __device__ __forceinline__ void upd_block2(double* S, int o, int rbA, int cbA, b
 // warp 0 updates the next 16x16 diagonal block and factors it right away while
 // warps 1-7 apply the rest of the rank-16 trailing update, so the sequential
 // 16-pivot kernels overlap the update work (2 consumer barriers per block).
+template <bool MULTI>
 __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
-                                   int* info, int* flag, int wr, int wc, int lane) {
+                                   int* info, int* flag, int wr, int wc, int lane, const DensePeers& pr) {
   const int tid = threadIdx.x, warp = tid >> 5;
   POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
@@ -420,17 +442,26 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
   // diagonal L tiles), publish, then L_jj (strict upper zeroed)
   for (int q = tid; q < 64 * 64; q += NCONS) {
     const int r = q >> 6, c = q & 63;
-    gLinvT[swz(r, c)] = S[(64 + r) * LSP + c];
+    const double v = S[(64 + r) * LSP + c];
+    gLinvT[swz(r, c)] = v;
+    if (MULTI)
+      for (int p = 0; p < pr.n; ++p) pr.LinvT[p][(size_t)j * TILE + swz(r, c)] = v;
   }
   if (flag) {
     fence_proxy_async_global();
-    __threadfence();
+    fence_tile_stores<MULTI>();
     cons_sync();
-    if (tid == 0) st_release(flag, 1);
+    if (tid == 0) {
+      st_release(flag, 1);
+      if (MULTI) release_peers(pr, tidx(j, j), 1);
+    }
   }
   for (int q = tid; q < 64 * 64; q += NCONS) {
     const int r = q >> 6, c = q & 63;
-    gL[swz(r, c)] = (c <= r) ? S[r * LSP + c] : 0.0;
+    const double v = (c <= r) ? S[r * LSP + c] : 0.0;
+    gL[swz(r, c)] = v;
+    if (MULTI)
+      for (int p = 0; p < pr.n; ++p) pr.L[p][(size_t)tidx(j, j) * TILE + swz(r, c)] = v;
   }
   POTRF_MARK(14)
 }
@@ -441,8 +472,8 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
 // mbarrier ring), so claim latency, the first tile's TMA latency and the
 // finalize overlap. Diagonal tasks factor in the stage area, so across them
 // the producer waits for the consumers (named barrier 2).
-__global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, const int2* __restrict__ tasks,
-                                                                int ntasks) {
+template <bool MULTI>
+__device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __restrict__ tasks, int ntasks) {
   extern __shared__ __align__(128) double smd[];
   CholSmem sm;
   sm.stage0 = smd;
@@ -483,7 +514,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       ++it;
     };
     auto wait_ready = [&](const int* f, int v) {
-      if (lane == 0) poll_flag(f, v);
+      if (lane == 0) poll_flag<MULTI>(f, v);
       __syncwarp();
     };
     // flag values: 1 = final; the sub-diagonal tile (k+1, k) is first
@@ -592,12 +623,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       double* scratch = sm.scratch;
       acc_to_swz(out, scratch, wr, wc, lane);
       acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+      if (MULTI)
+        for (int p = 0; p < d.peers.n; ++p)
+          acc_to_swz(out, d.peers.L[p] + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
       cons_sync();
       mma_abt<true>(acc, scratch, scratch, wr, wc, lane);  // its rank-64 update first ...
       fence_proxy_async_global();                          // ... then publish (the fence overlapped it)
-      __threadfence();
+      fence_tile_stores<MULTI>();
       cons_sync();
-      if (tid == 0) st_release(d.flags + tidx(j, j - 1), 2);
+      if (tid == 0) {
+        st_release(d.flags + tidx(j, j - 1), 2);
+        if (MULTI) release_peers(d.peers, tidx(j, j - 1), 2);
+      }
       if (lane == 0) {
         mbar_arrive(&sm.empty[sa]);
         mbar_arrive(&sm.empty[sb]);
@@ -607,8 +644,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
     if (d.trace && tid == 0) t_kdone = globaltimer();
     if (i == j) {
       // the producer is parked: the whole stage area holds the augmented panel + D^-T
-      potrf_blocked_tile(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
-                         d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane);
+      potrf_blocked_tile<MULTI>(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
+                                d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane, d.peers);
     } else if (i == j + 1 && !rhs) {
       // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
       acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
@@ -627,14 +664,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
       ++it;
       double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
       acc_to_swz(out, dst, wr, wc, lane);
+      if (MULTI)  // tile-cyclic: no RHS row
+        for (int p = 0; p < d.peers.n; ++p) acc_to_swz(out, d.peers.L[p] + (size_t)tidx(i, j) * TILE, wr, wc, lane);
     }
     if (d.trace && tid == 0) t_fin = globaltimer();
     fence_proxy_async_smem();    // generic smem writes before later bulk copies into the stages
     fence_proxy_async_global();  // generic global tile stores before other CTAs' bulk reads
-    __threadfence();
+    fence_tile_stores<MULTI>();
     cons_sync();  // every consumer's stores are fenced; the scratch tile is free again
     if (tid == 0) {
       st_release(myflag, 1);
+      // peers get final tiles only: the diagonal released its own, a partial
+      // (j+1, j) is finalized (flag 2) by the diagonal task j+1 on this rank
+      if (MULTI && i > j + 1) release_peers(d.peers, tidx(i, j), 1);
       if (d.trace) {
         unsigned long long* tr = d.trace + 4 * (size_t)task;
         tr[0] = t_claim;
@@ -645,6 +687,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, cons
     }
     if (i == j) asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");  // release the producer
   }
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_tiles(DenseDev d, const int2* __restrict__ tasks,
+                                                                int ntasks) {
+  cholesky_body<false>(d, tasks, ntasks);
+}
+
+// Tile-cyclic factorization: CTA b serves rank b % P (P = 1 on a real
+// multi-GPU rank, P = world size when one GPU emulates all ranks' replicas).
+__global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_ranks(const DenseRankJob* __restrict__ jobs, int P) {
+  const DenseRankJob& job = jobs[blockIdx.x % P];
+  cholesky_body<true>(job.d, job.tasks, job.ntasks);
 }
 
 // u = L^-T y, block rows from the bottom: x_j = (y_j - sum_{i>j} x_i L_ij) W_j
@@ -967,6 +1021,16 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
   k_cholesky_tiles<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
 }
 
+void launch_cholesky_ranks(cudaStream_t st, const DenseRankJob* jobs, int P, int grid) {
+  static bool attr = false;
+  size_t smem = cholesky_smem_bytes();
+  if (!attr) {
+    cudaFuncSetAttribute(k_cholesky_ranks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_cholesky_ranks<<<grid, NTHREADS, smem, st>>>(jobs, P);
+}
+
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u,
                            unsigned long long* trace) {
   static bool attr = false;
@@ -1012,6 +1076,21 @@ std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead) {
     if (with_rhs) tk.push_back(make_int2(N, j));
   }
   return tk;
+}
+
+// Tile-cyclic ownership: column j belongs to rank j mod P, except the
+// sub-diagonal partial (j+1, j), which belongs to the rank of diagonal j+1
+// (the diagonal task finalizes it, so the partial never leaves that rank).
+int dense_tile_owner(int i, int j, int nranks) { return (i == j + 1 ? i : j) % nranks; }
+
+// A rank's tasks in the global claim order: every cross-rank dependency
+// points to an earlier task of the global order, so with all ranks' CTAs
+// resident the globally first unfinished task always progresses.
+std::vector<int2> cholesky_rank_tasks(int N, int rank, int nranks, int lead) {
+  std::vector<int2> all = cholesky_task_order(N, false, lead), mine;
+  for (const int2& t : all)
+    if (dense_tile_owner(t.x, t.y, nranks) == rank) mine.push_back(t);
+  return mine;
 }
 
 }  // namespace spb

@@ -43,6 +43,17 @@ void launch_proxy_final(cudaStream_t st, const ProxyDev& px, const int4* tets, c
                         const double* target, double* partial);
 
 // ------------------------------------------------------------------ dense.cu
+// Tile-cyclic multi-GPU factorization (BASELINE config 4): every rank keeps a
+// full replica of L; the CTA that finishes a tile also stores it into each
+// peer's replica over NVLink (P2P stores through CUDA-IPC mappings) and
+// releases the peer's readiness flag at system scope. n = 0 on one GPU.
+constexpr int MAX_DENSE_PEERS = 7;
+struct DensePeers {
+  int n;
+  double* L[MAX_DENSE_PEERS];
+  double* LinvT[MAX_DENSE_PEERS];
+  int* flags[MAX_DENSE_PEERS];
+};
 struct DenseDev {
   int m, N;                  // order and tile count (T = 64)
   const double* sigma0;      // lower tiles, tile-major (diagonal tiles full)
@@ -62,11 +73,23 @@ struct DenseDev {
   const double* proxy_c;
   const uint8_t* active;
   unsigned long long* trace;  // optional: per task {claim, k-loop done, finalize done, sm}
+  DensePeers peers;           // replicas this rank also writes (tile-cyclic mode)
+};
+// one rank's share of a tile-cyclic factorization: its replica, peers and task list
+struct DenseRankJob {
+  DenseDev d;
+  const int2* tasks;
+  int ntasks;
 };
 int dense_tile_count(int N);
 size_t cholesky_smem_bytes();
 void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid);
 std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead);
+// P ranks (real: one job per process, P = 1 per launch; emulated: one launch
+// over all ranks' replicas, CTA b serving rank b % P)
+void launch_cholesky_ranks(cudaStream_t st, const DenseRankJob* jobs, int P, int grid);
+int dense_tile_owner(int i, int j, int nranks);
+std::vector<int2> cholesky_rank_tasks(int N, int rank, int nranks, int lead);
 constexpr int CHOL_LEAD = 2;
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u,
                            unsigned long long* trace = nullptr);
