@@ -339,6 +339,8 @@ def run_b200(args):
         "gpu_launches": launches, "setup_s": setup_s,
         "clocks": clk.summary(),
     }
+    if world == 1:
+        line["pcg_baseline"] = pcg_baseline(sim, args)
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sec, times = cpu_oracle_frames(sim, args.cpu_frames, threads)
@@ -348,6 +350,28 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def pcg_baseline(sim, args, frames: int = 3):
+    """The paper's §5.4 comparison on the same scene: the device Jacobi-PCG
+    solver (solve_frame_pcg, tol 1e-10) stepped from copies of the current
+    state through the public solver API; ms per frame (min over frames)."""
+    from paper_2008_01541_b200 import solver as sol
+
+    cfg = sol.SolverConfig(outer_iters=args.outer, inner_iters=args.inner, solver_kind="pcg",
+                           detection_cadence=sim.config.detection_cadence)
+    st = sim.state.copy()
+    sol.solve_frame(sim.model, sim.system, st, cfg)  # operator upload + warm-up
+    t, its = [], []
+    for _ in range(frames):
+        s2 = sim.state.copy()
+        t0 = time.perf_counter()
+        m = sol.solve_frame(sim.model, sim.system, s2, cfg)
+        t.append(time.perf_counter() - t0)
+        its.append(m.pcg_iterations)
+    return {"solver": "pcg (device, Jacobi, tol 1e-10, 3 coordinates)", "ms_per_frame": 1e3 * min(t),
+            "frames_per_s": 1.0 / min(t), "iterations_per_pass": max(its),
+            "note": "Simulation-level wall time (host buffers), same scene and state as the Schur frames"}
 
 
 def run_batch(args):

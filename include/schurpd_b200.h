@@ -14,6 +14,7 @@
  *   spb_ctx_step        <- solve_frame_schur                (solver.py:387-455)
  *                          incl. _finish_metrics            (solver.py:373-384)
  *   spb_ctx_set_pose    <- harness.Simulation.pose output   (harness.py:575-590)
+ *   spb_ctx_frame_pcg   <- solve_frame_pcg                  (solver.py:542-603)
  *   spb_ctx_set_state / spb_ctx_get_state
  *                       <- SolverState fields               (solver.py:116-145)
  *   spb_op_*            <- the public per-op helpers of the hot path:
@@ -197,6 +198,22 @@ int32_t spb_ctx_step(spb_ctx *ctx, const spb_step_config *cfg, spb_frame_metrics
 int32_t spb_ctx_frame(spb_ctx *ctx, const double *att_targets, int32_t num_colliders,
                       const spb_posed_collider *colliders, double *x, uint8_t *active, double *target,
                       const spb_step_config *cfg, double *f_tilde2, double *u2_accum, spb_frame_metrics *metrics);
+/* PCG baseline (reference solve_frame_pcg, solver.py:542-603; the paper's
+ * §5.4 comparison solver), on the device. spb_ctx_set_operator hands over the
+ * global matrix A (reference GlobalSystem.A: upper CSC in partition order,
+ * n x n scalar); spb_ctx_frame_pcg then runs one frame like spb_ctx_frame:
+ * per inner pass A_col = A + C22 (active set), b = all-element elastic +
+ * attachment + collision forces, three Jacobi-PCG solves (one per coordinate,
+ * |r|/|b| <= tol or max_iters) in one cooperative launch, x += dx.
+ * pcg_iterations = worst per-pass count; metrics->residual = max_c
+ * |A_col dx_c - b_c| / |b_c| of the last pass. p'Ap <= 0 returns
+ * SPB_ERR_INDEFINITE with metrics->info = -1 (IndefiniteOperatorError). */
+int32_t spb_ctx_set_operator(spb_ctx *ctx, int64_t n, const int64_t *indptr, const int64_t *indices,
+                             const double *data);
+int32_t spb_ctx_frame_pcg(spb_ctx *ctx, const double *att_targets, int32_t num_colliders,
+                          const spb_posed_collider *colliders, double *x, uint8_t *active, double *target,
+                          const spb_step_config *cfg, double tol, int64_t max_iters, spb_frame_metrics *metrics,
+                          int64_t *pcg_iterations);
 /* Download state; any pointer may be NULL to skip that field. */
 int32_t spb_ctx_get_state(spb_ctx *ctx, double *x, double *R, double *Q, uint8_t *active, double *target,
                           double *f_tilde2, double *u2_accum);

@@ -110,6 +110,8 @@ _SIGS = {
     "spb_op_dense_solve": ([I64, P, I64, P, P], I32),
     "spb_op_forward_sub": ([P, I64, P, P, P, P], I32),
     "spb_op_backward_sub": ([P, I64, P, P, P], I32),
+    "spb_ctx_set_operator": ([P, I64, P, P, P], I32),
+    "spb_ctx_frame_pcg": ([P, P, I32, P, P, P, P, P, F64, I64, P, P], I32),
     "spb_dense_create": ([I64, I32, I32, I32, I32, P], I32),
     "spb_dense_destroy": ([P], None),
     "spb_dense_set_matrix": ([P, P], I32),

@@ -148,10 +148,16 @@ struct Ctx {
   DBuf<double> e_part, a_part, p_part, r_part, metrics_out;
   double* metrics_host = nullptr;    // pinned
   int e_blocks = 0, a_blocks = 0, p_blocks = 0, r_blocks = 0;
-  // early-exit (lazily built)
-  bool have_all_gather = false;
-  DBuf<double> Gall, fall;
-  DBuf<int> gall_ptr, gall_src, att_ptr_node, att_idx_node, node_ids;
+  // PCG baseline (built by spb_ctx_set_operator)
+  std::vector<int> fac_h, pl_h;      // factor-order key -> node; proxy slot -> x2-local id
+  bool have_pcg = false;
+  int pcg_nnz = 0, pcg_nent = 0;
+  DBuf<int> pcg_rowptr, pcg_col, pcg_pos, pcg_eptr, pcg_contrib, pcg_diag, gall_ptr, gall_src, zeros_n2;
+  DBuf<double> Gall, pcg_aval, pcg_val, pcg_dinv, pcg_vec, pcg_partial, pcg_resid;
+  DBuf<unsigned> pcg_bar;
+  DBuf<int> pcg_iters, pcg_track;
+  int* pcg_host = nullptr;           // pinned: track[2] (max iterations, error iteration)
+  double* pcg_resid_host = nullptr;  // pinned: [3]
   // graph cache
   std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>> graphs;  // solve, metrics
   int last_launches = 0;
@@ -170,6 +176,8 @@ struct Ctx {
     if (io_host) cudaFreeHost(io_host);
     sweep_work_free(sw);
     if (metrics_host) cudaFreeHost(metrics_host);
+    if (pcg_host) cudaFreeHost(pcg_host);
+    if (pcg_resid_host) cudaFreeHost(pcg_resid_host);
     if (ev_state) cudaEventDestroy(ev_state);
     if (st_io) cudaStreamDestroy(st_io);
     if (st) cudaStreamDestroy(st);
@@ -179,6 +187,8 @@ struct Ctx {
   // one frame = solve (outer/inner passes, state final) + metrics
   int enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev /* 6 phase events or null */);
   int enqueue_metrics(cudaEvent_t* ev);
+  int build_pcg(int64_t nrows, const int64_t* Ap, const int64_t* Ai, const double* Ax);
+  int enqueue_pcg(int outer, int inner, int cadence, double tol, int max_iters);
   int sync_shapes();
   int io_reserve(size_t bytes) {
     if (bytes <= io_bytes) return SPB_OK;
@@ -308,6 +318,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   for (int k = 0; k < n2; ++k) fac[n1 + k] = (int)order[n1 + k];
   for (int k = 0; k < n; ++k) key_of_node[fac[k]] = k;
   TRY(fac_node.upload(fac));
+  fac_h = fac;
   std::vector<int> x1n(fac.begin(), fac.begin() + n1), x2n(fac.begin() + n1, fac.end());
   TRY(x1_node.upload(x1n));
   TRY(x2_ids.upload(x2n));
@@ -362,6 +373,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   TRY(gc_src.upload(gc.src));
   TRY(prox_elem.upload(pe));
   TRY(prox_local.upload(pl));
+  pl_h = pl;
   TRY(prox_w.upload(s->proxy_weights, 4 * (size_t)P));
   TRY(prox_c.upload(s->proxy_stiffness, P));
   TRY(active.zeros(std::max(P, 1)));
@@ -533,6 +545,155 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       launches++;
     }
     if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[4], st));
+  }
+  last_launches = launches;
+  return SPB_OK;
+}
+
+// ---------------------------------------------------------- PCG baseline
+// A (reference system.A: upper CSC, partition order) -> full CSR in factor
+// order, the C22 entry lists of every proxy pair (merged into A's pattern),
+// the all-element force gather, and the CG vectors.
+int Ctx::build_pcg(int64_t nrows, const int64_t* Ap, const int64_t* Ai, const double* Ax) {
+  if (nrows != n) { set_error("operator order differs from the scene's node count"); return SPB_ERR_ARG; }
+  // partition index -> key: partition index p is node order[p]; key_of_node[fac[k]] = k
+  std::vector<int> order_h(n), key_of_node(n);
+  for (int64_t k = 0; k < n; ++k) key_of_node[fac_h[k]] = (int)k;
+  // the partition order of x1 is recovered from the factor's fill order:
+  // fac[k] = order[fill_perm[k]] (k < n1), fac[n1 + k] = order[n1 + k]
+  for (int64_t k = 0; k < n1; ++k) order_h[factor->fill_perm[k]] = fac_h[k];
+  for (int64_t k = n1; k < n; ++k) order_h[k] = fac_h[k];
+  std::vector<std::vector<std::pair<int, double>>> rows(n);
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t q = Ap[c]; q < Ap[c + 1]; ++q) {
+      const int64_t r = Ai[q];
+      if (r < 0 || r > c) { set_error("operator must be upper-triangular CSC"); return SPB_ERR_ARG; }
+      const int kr = key_of_node[order_h[r]], kc = key_of_node[order_h[c]];
+      rows[kr].emplace_back(kc, Ax[q]);
+      if (r != c) rows[kc].emplace_back(kr, Ax[q]);
+    }
+  // C22 pattern: upper (ra <= cb) contributions in (proxy, a, b) order, mirrored
+  std::map<std::pair<int, int>, std::vector<int>> ent;
+  for (int j = 0; j < P; ++j)
+    for (int a = 0; a < 4; ++a)
+      for (int bb = 0; bb < 4; ++bb) {
+        const int ra = pl_h[4 * j + a], cb = pl_h[4 * j + bb];
+        if (ra > cb) continue;
+        ent[{n1 + ra, n1 + cb}].push_back(j * 16 + a * 4 + bb);
+        if (ra != cb) ent[{n1 + cb, n1 + ra}].push_back(j * 16 + a * 4 + bb);
+      }
+  for (auto& kv : ent) rows[kv.first.first].emplace_back(kv.first.second, 0.0);  // pattern union
+  std::vector<int> rp(n + 1, 0), ci, diag(n, -1);
+  std::vector<double> av;
+  for (int64_t i = 0; i < n; ++i) {
+    auto& r = rows[i];
+    std::sort(r.begin(), r.end(), [](const std::pair<int, double>& u, const std::pair<int, double>& v) {
+      return u.first < v.first;
+    });
+    for (size_t k = 0; k < r.size(); ++k) {
+      if (!ci.empty() && (int)ci.size() > rp[i] && ci.back() == r[k].first) {
+        av.back() += r[k].second;  // duplicate (pattern union zeros)
+        continue;
+      }
+      if (r[k].first == i) diag[i] = (int)ci.size();
+      ci.push_back(r[k].first);
+      av.push_back(r[k].second);
+    }
+    rp[i + 1] = (int)ci.size();
+    if (diag[i] < 0) { set_error("operator has an empty diagonal entry"); return SPB_ERR_ARG; }
+  }
+  std::vector<int> pos, eptr(1, 0), codes;
+  for (auto& kv : ent) {
+    const int i = kv.first.first, c = kv.first.second;
+    const int* b0 = ci.data() + rp[i];
+    const int* hit = std::lower_bound(b0, (const int*)ci.data() + rp[i + 1], c);
+    pos.push_back((int)(hit - ci.data()));
+    codes.insert(codes.end(), kv.second.begin(), kv.second.end());
+    eptr.push_back((int)codes.size());
+  }
+  pcg_nnz = (int)ci.size();
+  pcg_nent = (int)pos.size();
+  TRY(pcg_rowptr.upload(rp));
+  TRY(pcg_col.upload(ci));
+  TRY(pcg_aval.upload(av));
+  TRY(pcg_val.alloc(av.size()));
+  TRY(pcg_diag.upload(diag));
+  TRY(pcg_pos.upload(pos.empty() ? std::vector<int>{0} : pos));
+  TRY(pcg_eptr.upload(eptr));
+  TRY(pcg_contrib.upload(codes.empty() ? std::vector<int>{0} : codes));
+  TRY(pcg_dinv.alloc(n));
+  TRY(pcg_vec.zeros(6 * 3 * (size_t)n));
+  TRY(pcg_partial.zeros(pcg_partial_doubles()));
+  TRY(pcg_resid.zeros(3));
+  TRY(pcg_bar.zeros(1));
+  TRY(pcg_iters.zeros(4));
+  TRY(pcg_track.zeros(2));
+  TRY(zeros_n2.zeros((size_t)n2 + 1));
+  // all-element node gather in factor order (reference _pose_forces: every element)
+  std::vector<int4> t4(ne);
+  SPB_CUDA(cudaMemcpy(t4.data(), tets.p, sizeof(int4) * ne, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> th(4 * ne);
+  for (int64_t e = 0; e < ne; ++e) {
+    th[4 * e] = t4[e].x; th[4 * e + 1] = t4[e].y; th[4 * e + 2] = t4[e].z; th[4 * e + 3] = t4[e].w;
+  }
+  Csr ga = element_gather(th, nullptr, ne, key_of_node, (int)n);
+  TRY(gall_ptr.upload(ga.ptr));
+  TRY(gall_src.upload(ga.src));
+  TRY(Gall.alloc(12 * (size_t)ne));
+  if (!pcg_host) SPB_CUDA(cudaMallocHost(&pcg_host, sizeof(int) * 4));
+  if (!pcg_resid_host) SPB_CUDA(cudaMallocHost(&pcg_resid_host, sizeof(double) * 3));
+  SPB_CUDA(cudaDeviceSynchronize());
+  have_pcg = true;
+  return SPB_OK;
+}
+
+__global__ void k_pcg_track(const int* __restrict__ iters, int* __restrict__ track) {
+  if (threadIdx.x == 0) {
+    track[0] = max(track[0], max(iters[0], max(iters[1], iters[2])));
+    if (iters[3] && !track[1]) track[1] = iters[3];
+  }
+}
+
+// solve_frame_pcg (reference solver.py:542-603), one device enqueue per frame
+int Ctx::enqueue_pcg(int outer, int inner, int cadence, double tol, int max_iters) {
+  if (!have_pcg) { set_error("PCG needs the operator (spb_ctx_set_operator)"); return SPB_ERR_ARG; }
+  int launches = 0;
+  const ProxyDev P_ = px();
+  bool first_detection_done = false;
+  residual_valid = false;
+  SPB_CUDA(cudaMemsetAsync(pcg_track.p, 0, sizeof(int) * 2, st));
+  SPB_CUDA(cudaMemsetAsync(pcg_resid.p, 0, sizeof(double) * 3, st));
+  double* V = pcg_vec.p;
+  const size_t n3 = 3 * (size_t)n;
+  PcgDev d{(int)n, pcg_rowptr.p, pcg_col.p, pcg_val.p, pcg_dinv.p, V, V + n3, V + 2 * n3, V + 3 * n3,
+           V + 4 * n3, V + 5 * n3, pcg_partial.p, pcg_bar.p, tol, max_iters, pcg_iters.p, pcg_resid.p};
+  for (int o = 0; o < outer; ++o) {
+    launch_local_forces(st, nalpha, e_alpha.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, nullptr, 1);
+    launches += nalpha > 0;
+    for (int it = 0; it < inner; ++it) {
+      bool fresh = cadence == SPB_CADENCE_INNER || (cadence == SPB_CADENCE_FRAME && !first_detection_done);
+      if (fresh && P > 0) {
+        launch_detect(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
+        launches++;
+      }
+      first_detection_done = true;
+      launch_local_forces(st, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, nullptr, 1);
+      // A_col = A + C22 (active set), Jacobi diagonal
+      TRY(launch_pcg_values(st, pcg_nnz, pcg_aval.p, pcg_val.p, pcg_nent, pcg_pos.p, pcg_eptr.p, pcg_contrib.p,
+                            prox_w.p, prox_c.p, active.p, (int)n, pcg_diag.p, pcg_dinv.p));
+      // b = _pose_forces: every element (current R/Q) + attachments, then collisions
+      launch_local_forces(st, (int)ne, nullptr, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gall.p, 0);
+      launch_gather_forces(st, (int)n, gall_ptr.p, gall_src.p, Gall.p, (int)ne, fac_node.p, att_ptr.p, att_idx.p,
+                           att_k.p, att_tgt.p, x.p, V);
+      if (n2 > 0)
+        launch_build_g(st, n2, V + 3 * (size_t)n1, zeros_n2.p, zeros_n2.p, Gall.p, 1, P_, tets.p, x.p, active.p,
+                       target.p, gc_ptr.p, gc_src.p, V + 3 * (size_t)n1, nullptr);
+      SPB_CUDA(cudaMemsetAsync(pcg_iters.p, 0, sizeof(int) * 4, st));
+      TRY(launch_pcg(st, d));
+      k_pcg_track<<<1, 32, 0, st>>>(pcg_iters.p, pcg_track.p);
+      launch_scatter_add(st, (int)n, fac_node.p, d.x, x.p);
+      launches += (nbeta > 0) + 2 + (pcg_nent > 0) + 1 + 1 + (n2 > 0) + 1 + 1 + 1;
+    }
   }
   last_launches = launches;
   return SPB_OK;
@@ -829,6 +990,64 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
   TRY(io_download(c, down, c->st_io, true));
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return frame_finish(c, m);
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_set_operator(spb_ctx* cp, int64_t n, const int64_t* indptr, const int64_t* indices,
+                             const double* data) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  if (!c || !indptr || !indices || !data) { spb::set_error("spb_ctx_set_operator: null argument"); return SPB_ERR_ARG; }
+  SPB_CUDA(cudaSetDevice(c->device));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  return c->build_pcg(n, indptr, indices, data);
+  SPB_GUARD_END
+}
+
+int32_t spb_ctx_frame_pcg(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
+                          double* x, uint8_t* active, double* target, const spb_step_config* cfg, double tol,
+                          int64_t max_iters, spb_frame_metrics* m, int64_t* pcg_iterations) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  auto t0 = std::chrono::steady_clock::now();
+  memset(m, 0, sizeof(*m));
+  if (cfg->outer_iters < 1 || cfg->inner_iters < 1 || max_iters < 1 || max_iters > (1 << 30) || !(tol >= 0.0)) {
+    spb::set_error("spb_ctx_frame_pcg: bad iteration counts or tolerance");
+    return SPB_ERR_ARG;
+  }
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  TRY(pose_upload(c, att_targets, ncol, cols));
+  IoList up;
+  up.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  if (c->P) up.add(c->active.p, active, c->P);
+  if (c->P) up.add(c->target.p, target, sizeof(double) * 3 * c->P);
+  TRY(io_upload(c, up, false));
+  TRY(c->sync_shapes());
+  TRY(c->enqueue_pcg(cfg->outer_iters, cfg->inner_iters, cfg->cadence, tol, (int)max_iters));
+  SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
+  TRY(c->enqueue_metrics(nullptr));
+  SPB_CUDA(cudaMemcpyAsync(c->metrics_host, c->metrics_out.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
+  SPB_CUDA(cudaMemcpyAsync(c->pcg_host, c->pcg_track.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->st));
+  SPB_CUDA(cudaMemcpyAsync(c->pcg_resid_host, c->pcg_resid.p, sizeof(double) * 3, cudaMemcpyDeviceToHost, c->st));
+  IoList down;
+  down.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  if (c->P) down.add(c->active.p, active, c->P);
+  if (c->P) down.add(c->target.p, target, sizeof(double) * 3 * c->P);
+  TRY(io_download(c, down, c->st_io, true));
+  m->energy = c->metrics_host[0];
+  m->max_penetration = c->metrics_host[1];
+  m->active_proxies = (int64_t)llround(c->metrics_host[3]);
+  m->residual = std::max(c->pcg_resid_host[0], std::max(c->pcg_resid_host[1], c->pcg_resid_host[2]));
+  m->kernel_launches = c->last_launches;
+  if (pcg_iterations) *pcg_iterations = c->pcg_host[0];
+  m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (c->pcg_host[1] > 0) {
+    m->info = -1;
+    spb::set_error("p'Ap <= 0 at PCG iteration " + std::to_string(c->pcg_host[1]) + ": operator not positive definite");
+    return SPB_ERR_INDEFINITE;
+  }
+  return SPB_OK;
   SPB_GUARD_END
 }
 

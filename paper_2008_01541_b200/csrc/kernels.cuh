@@ -96,6 +96,29 @@ void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, do
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial);
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out);
 
+// -------------------------------------------------------------------- pcg.cu
+struct PcgDev {
+  int n;                                     // rows (context factor order)
+  const int* rowptr;
+  const int* col;
+  const double* val;                         // A + C22, full CSR
+  const double* dinv;                        // Jacobi: 1 / diag
+  const double* b;                           // (n,3)
+  double *x, *r, *z, *p, *q;                 // (n,3)
+  double* partial;                           // pcg_partial_doubles()
+  unsigned* bar;                             // grid barrier counter
+  double tol;
+  int max_iters;
+  int* iters;                                // [3] per column, [3] = iteration of a p'Ap <= 0 (0: none)
+  double* resid;                             // [3] |A x - b| / |b|
+};
+int pcg_grid();
+size_t pcg_partial_doubles();
+int launch_pcg_values(cudaStream_t st, int nnz, const double* aval, double* val, int nent, const int* pos,
+                      const int* eptr, const int* contrib, const double* w, const double* cst,
+                      const uint8_t* active, int n, const int* diag_pos, double* dinv);
+int launch_pcg(cudaStream_t st, const PcgDev& d);
+
 // ----------------------------------------------------------------- sparse.cu
 struct DeviceFactor;
 int build_device_factor(Factor& f);

@@ -1,0 +1,315 @@
+// Jacobi-preconditioned CG on the collision-augmented operator, on the device:
+// the comparison solver of the paper's §5.4 (reference solver.py:542-603
+// solve_frame_pcg, linalg.py pcg). The operator A_col = A + C22 (reference
+// _collision_augmented, solver.py:456-464) is a full scalar CSR in the
+// context's factor order (a symmetric permutation of the reference's
+// partition order: CG is invariant under it up to rounding); the three
+// coordinates are three independent CG runs, each with its own step sizes,
+// stopping test |r| / |b| <= tol and iteration count, exactly as the reference
+// loops `for c in range(3)`.
+//
+// One cooperative persistent launch runs a whole solve (all iterations), so a
+// pass costs no host round trip. Per iteration two grid barriers:
+//   (1) alpha = rz / p.q; x += alpha p; r -= alpha q; z = D^-1 r; partial r.r, r.z
+//   (2) convergence test; beta = rz'/rz; q = A z + beta q; p = z + beta p; partial p.q
+// q = A z + beta q equals A (z + beta p) and keeps the update row-local, so p
+// never needs a barrier of its own. Reductions are fixed-order (per-block tree,
+// then every block sums the block partials in the same order): bit-identical
+// replays, and every block takes the same branch at the stopping test.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace spb {
+
+namespace {
+constexpr int PCG_THREADS = 256;
+constexpr int NPART = 8;  // partial slots per block
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All blocks are co-resident (cooperative launch); the counter only grows.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire_u32(bar) < target) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
+// Block tree over K values per thread -> partial[block][k] (fixed order).
+template <int K>
+__device__ __forceinline__ void block_partials(const double (&v)[K], double* partial, double* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double s = v[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sm[warp * NPART + k] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double s = 0.0;
+    for (int w = 0; w < PCG_THREADS / 32; ++w) s += sm[w * NPART + threadIdx.x];
+    partial[(size_t)blockIdx.x * NPART + threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Every block: out[k] = sum over blocks of partial[b][k], same order everywhere.
+template <int K>
+__device__ __forceinline__ void grid_sums(const double* partial, double* out /* smem[K] */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < K) {
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += partial[(size_t)b * NPART + warp];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[warp] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void spmv_row(const PcgDev& d, int i, const double* __restrict__ v, double& s0,
+                                         double& s1, double& s2) {
+  s0 = s1 = s2 = 0.0;
+  for (int e = d.rowptr[i]; e < d.rowptr[i + 1]; ++e) {
+    const double a = d.val[e];
+    const int c = d.col[e];
+    s0 = fma(a, v[3 * c + 0], s0);
+    s1 = fma(a, v[3 * c + 1], s1);
+    s2 = fma(a, v[3 * c + 2], s2);
+  }
+}
+
+__global__ void __launch_bounds__(PCG_THREADS) k_pcg(PcgDev d) {
+  __shared__ double sm[(PCG_THREADS / 32) * NPART];
+  __shared__ double red[NPART];
+  __shared__ double s_rz[3], s_bn[3], s_alpha[3], s_beta[3];
+  __shared__ int s_done[3], s_stop;
+  unsigned target = 0;
+  const int n = d.n;
+  const int stride = gridDim.x * PCG_THREADS;
+  const int t0 = blockIdx.x * PCG_THREADS + threadIdx.x;
+
+  // ---- x = 0, r = b, z = D^-1 r, p = z; partials r.z, b.b
+  {
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = t0; i < n; i += stride) {
+      const double di = d.dinv[i];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double bi = d.b[3 * i + c];
+        const double zi = di * bi;
+        d.x[3 * i + c] = 0.0;
+        d.r[3 * i + c] = bi;
+        d.z[3 * i + c] = zi;
+        d.p[3 * i + c] = zi;
+        v[c] += bi * zi;
+        v[3 + c] += bi * bi;
+      }
+    }
+    block_partials<6>(v, d.partial, sm);
+  }
+  grid_barrier(d.bar, target);
+  grid_sums<6>(d.partial, red);
+  if (threadIdx.x < 3) {
+    const int c = threadIdx.x;
+    s_rz[c] = red[c];
+    s_bn[c] = sqrt(red[3 + c]);
+    s_done[c] = s_bn[c] == 0.0;  // reference: |b| = 0 -> x = 0, 0 iterations
+    if (blockIdx.x == 0) d.iters[c] = 0;
+  }
+  __syncthreads();
+  // ---- q = A p; partial p.q
+  {
+    double v[3] = {0, 0, 0};
+    for (int i = t0; i < n; i += stride) {
+      double q0, q1, q2;
+      spmv_row(d, i, d.p, q0, q1, q2);
+      d.q[3 * i + 0] = q0;
+      d.q[3 * i + 1] = q1;
+      d.q[3 * i + 2] = q2;
+      v[0] += d.p[3 * i + 0] * q0;
+      v[1] += d.p[3 * i + 1] * q1;
+      v[2] += d.p[3 * i + 2] * q2;
+    }
+    block_partials<3>(v, d.partial, sm);
+  }
+  grid_barrier(d.bar, target);
+  int it = 1;
+  for (; it <= d.max_iters; ++it) {
+    // ---- (1) step along p
+    grid_sums<3>(d.partial, red);
+    if (threadIdx.x == 0) {
+      s_stop = 0;
+      for (int c = 0; c < 3; ++c) {
+        s_alpha[c] = 0.0;
+        if (s_done[c]) continue;
+        const double pq = red[c];
+        if (pq <= 0.0) {  // reference: IndefiniteOperatorError
+          s_stop = 1;
+          if (blockIdx.x == 0) d.iters[3] = it;
+        } else {
+          s_alpha[c] = s_rz[c] / pq;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    {
+      double v[6] = {0, 0, 0, 0, 0, 0};
+      for (int i = t0; i < n; i += stride) {
+        const double di = d.dinv[i];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (s_done[c]) continue;
+          const double a = s_alpha[c];
+          const int k = 3 * i + c;
+          d.x[k] += a * d.p[k];
+          const double rk = d.r[k] - a * d.q[k];
+          d.r[k] = rk;
+          const double zk = di * rk;
+          d.z[k] = zk;
+          v[c] += rk * rk;
+          v[3 + c] += rk * zk;
+        }
+      }
+      block_partials<6>(v, d.partial, sm);
+    }
+    grid_barrier(d.bar, target);
+    // ---- (2) stopping test, new direction
+    grid_sums<6>(d.partial, red);
+    if (threadIdx.x == 0) {
+      int all = 1;
+      for (int c = 0; c < 3; ++c) {
+        s_beta[c] = 0.0;
+        if (s_done[c]) continue;
+        if (sqrt(red[c]) / s_bn[c] <= d.tol) {
+          s_done[c] = 1;
+          if (blockIdx.x == 0) d.iters[c] = it;
+          continue;
+        }
+        all = 0;
+        s_beta[c] = red[3 + c] / s_rz[c];
+        s_rz[c] = red[3 + c];
+      }
+      s_stop = all;
+    }
+    __syncthreads();
+    if (s_stop) break;
+    {
+      double v[3] = {0, 0, 0};
+      for (int i = t0; i < n; i += stride) {
+        double s[3];
+        spmv_row(d, i, d.z, s[0], s[1], s[2]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (s_done[c]) continue;
+          const int k = 3 * i + c;
+          const double bt = s_beta[c];
+          const double qk = s[c] + bt * d.q[k];
+          const double pk = d.z[k] + bt * d.p[k];
+          d.q[k] = qk;
+          d.p[k] = pk;
+          v[c] += pk * qk;
+        }
+      }
+      block_partials<3>(v, d.partial, sm);
+    }
+    grid_barrier(d.bar, target);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 3 && !s_done[threadIdx.x] && !s_stop) d.iters[threadIdx.x] = d.max_iters;
+  // ---- residual |A x - b| / |b| per column (reference :588-590)
+  grid_barrier(d.bar, target);  // x complete everywhere
+  {
+    double v[3] = {0, 0, 0};
+    for (int i = t0; i < n; i += stride) {
+      double s[3];
+      spmv_row(d, i, d.x, s[0], s[1], s[2]);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double e = s[c] - d.b[3 * i + c];
+        v[c] += e * e;
+      }
+    }
+    block_partials<3>(v, d.partial, sm);
+  }
+  grid_barrier(d.bar, target);
+  grid_sums<3>(d.partial, red);
+  if (blockIdx.x == 0 && threadIdx.x < 3) {
+    const int c = threadIdx.x;
+    d.resid[c] = s_bn[c] > 0.0 ? sqrt(red[c]) / s_bn[c] : 0.0;
+  }
+}
+
+// val = A + C22 from the live active set: each x2-block entry adds its active
+// contributions c_j w_a w_b in the reference's COO order (collision.py:401-434)
+__global__ void k_pcg_values(int nent, const int* __restrict__ pos, const int* __restrict__ eptr,
+                             const int* __restrict__ contrib, const double* __restrict__ aval,
+                             const double* __restrict__ w, const double* __restrict__ cst,
+                             const uint8_t* __restrict__ active, double* __restrict__ val) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nent) return;
+  double s = 0.0;
+  bool any = false;
+  for (int q = eptr[e]; q < eptr[e + 1]; ++q) {
+    const int code = contrib[q];
+    const int j = code >> 4, a = (code >> 2) & 3, b = code & 3;
+    if (!active[j]) continue;
+    const double v = cst[j] * (w[4 * j + a] * w[4 * j + b]);
+    s = any ? s + v : v;
+    any = true;
+  }
+  const int p = pos[e];
+  val[p] = any ? aval[p] + s : aval[p];
+}
+
+__global__ void k_pcg_jacobi(int n, const int* __restrict__ diag_pos, const double* __restrict__ val,
+                             double* __restrict__ dinv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dinv[i] = 1.0 / val[diag_pos[i]];
+}
+}  // namespace
+
+int pcg_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg, PCG_THREADS, 0);
+    int dev = 0, sms = NUM_SMS_B200;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::max(1, std::min(per_sm, 2)) * sms;
+  }
+  return grid;
+}
+
+size_t pcg_partial_doubles() { return (size_t)pcg_grid() * NPART; }
+
+int launch_pcg_values(cudaStream_t st, int nnz, const double* aval, double* val, int nent, const int* pos,
+                      const int* eptr, const int* contrib, const double* w, const double* cst,
+                      const uint8_t* active, int n, const int* diag_pos, double* dinv) {
+  SPB_CUDA(cudaMemcpyAsync(val, aval, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
+  if (nent > 0) k_pcg_values<<<ceil_div(nent, 256), 256, 0, st>>>(nent, pos, eptr, contrib, aval, w, cst, active, val);
+  k_pcg_jacobi<<<ceil_div(n, 256), 256, 0, st>>>(n, diag_pos, val, dinv);
+  SPB_CUDA(cudaGetLastError());
+  return SPB_OK;
+}
+
+int launch_pcg(cudaStream_t st, const PcgDev& d) {
+  SPB_CUDA(cudaMemsetAsync(d.bar, 0, sizeof(unsigned), st));
+  PcgDev arg = d;
+  void* args[] = {&arg};
+  SPB_CUDA(cudaLaunchCooperativeKernel((void*)k_pcg, dim3(pcg_grid()), dim3(PCG_THREADS), args, 0, st));
+  return SPB_OK;
+}
+
+}  // namespace spb

@@ -16,6 +16,8 @@ Fixtures (all small, np.savez_compressed):
                  cadence, biphasic) configurations (solver.py:387-455)
   cfg1.npz       BASELINE config 1 (beam 20x8x8, proxies on x in [0.7,1.3] of the
                  top face), 50 frames through Simulation.step()
+  bar_pcg.npz    the PCG baseline (solver.py:542-603) on the bar fixture:
+                 pre/post states and iteration counts
   hinge.npz      built-in hinge_fold scene (capsule collider, rotating
                  attachments, outer=2 inner=2), 24 frames
   setup hashes   sha256 of every setup array, so the product's own host-side
@@ -222,6 +224,25 @@ def gen_bar(name, biphasic, outer, inner, cadence, frames, press_depth=0.08, jit
     print(name, "m =", part.n2, "active", state.active.count)
 
 
+def gen_bar_pcg(name, outer, inner, cadence, frames, press_depth=0.08, tol=1e-10):
+    """The PCG baseline (solver.py:542-603) on the same bar: pre/post states
+    and the worst per-pass iteration count of every frame."""
+    model, system, state, part = make_scene(press_depth=press_depth)
+    cfg = sol.SolverConfig(outer_iters=outer, inner_iters=inner, detection_cadence=cadence, solver_kind="pcg",
+                           pcg_tol=tol)
+    out = {"outer": outer, "inner": inner, "cadence": cadence, "press_depth": press_depth, "frames": frames,
+           "tol": tol}
+    for f in range(frames):
+        pre = state.copy()
+        met = sol.solve_frame_pcg(model, system, state, cfg)
+        out.update(_state_dict(f"pre{f}_", pre, rotations=False))
+        out.update(_state_dict(f"post{f}_", state, rotations=False))
+        out[f"metrics{f}"] = _metrics_vec(met)
+        out[f"iters{f}"] = met.pcg_iterations
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+    print(name, "m =", part.n2, "iters", [int(out[f"iters{f}"]) for f in range(frames)])
+
+
 # ----------------------------------------------------------------- scenes
 
 
@@ -294,6 +315,9 @@ def gen_partial_factor():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["pcg"]:  # only the PCG-baseline fixture
+        gen_bar_pcg("bar_pcg", 1, 2, "inner", 3)
+        sys.exit(0)
     gen_svd()
     gen_detect()
     gen_bar("bar_plain", False, 1, 1, "inner", 5)
@@ -304,3 +328,4 @@ if __name__ == "__main__":
     hinge = harness.builtin_scene_path("hinge_fold").read_text()
     gen_scene("hinge", hinge, 24, every=6)
     gen_partial_factor()
+    gen_bar_pcg("bar_pcg", 1, 2, "inner", 3)
