@@ -408,7 +408,8 @@ __device__ __forceinline__ double bw_gather_q(int p, int q, const int* __restric
 // CTA task (s, r0): rows r0 .. r0 + R - 1, R in {8, ..., 128}: lanes cover
 // RL = min(R, 32) rows x 32/RL column subgroups, warps cover G = R/32 row
 // groups x 16/G column groups; every thread strides its column group.
-__global__ void __launch_bounds__(FW_THREADS) k_fw_level(
+template <int FW_BATCH, int FW_MINB>
+__global__ void __launch_bounds__(FW_THREADS, FW_MINB) k_fw_level(
     const SnDev* __restrict__ sn, const double* __restrict__ M, const int2* __restrict__ cta_tasks, int ncta,
     const int2* __restrict__ warp_tasks, int nwarp, int R, const double* __restrict__ V, double* __restrict__ y,
     double* __restrict__ U) {
@@ -435,14 +436,26 @@ __global__ void __launch_bounds__(FW_THREADS) k_fw_level(
       for (int e = threadIdx.x; e < 3 * (c1 - c0); e += FW_THREADS) sm[e] = Vs[3 * c0 + e];
       __syncthreads();
       if (valid) {
-        int c = c0 + cgi;
-#pragma unroll 16
-        for (; c < c1; c += ncg) {
-          const double mv = Mp[(int64_t)c * S.nr];
-          const double* v = sm + 3 * (c - c0);
-          a0 += mv * v[0];
-          a1 += mv * v[1];
-          a2 += mv * v[2];
+        // predicated batches of FW_BATCH loads: every batch (the last,
+        // partial one included) keeps FW_BATCH panel loads in flight; the
+        // accumulation order (c ascending) is unchanged
+        for (int cb = c0 + cgi; cb < c1; cb += FW_BATCH * ncg) {
+          double mv[FW_BATCH];
+#pragma unroll
+          for (int u = 0; u < FW_BATCH; ++u) {
+            const int c = cb + u * ncg;
+            mv[u] = c < c1 ? Mp[(int64_t)c * S.nr] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < FW_BATCH; ++u) {
+            const int c = cb + u * ncg;
+            if (c < c1) {
+              const double* v = sm + 3 * (c - c0);
+              a0 += mv[u] * v[0];
+              a1 += mv[u] * v[1];
+              a2 += mv[u] * v[2];
+            }
+          }
         }
       }
     }
@@ -502,6 +515,24 @@ __global__ void __launch_bounds__(FW_THREADS) k_fw_level(
         U[o + 2] = Vs[3 * r + 2] - a2;
       }
     }
+  }
+}
+
+// k_fw_level variants: panel loads in flight per thread x resident CTAs per SM
+// (SPB_FW_VARIANT for diagnostics; the level task heights follow the slots)
+using FwLevelFn = void (*)(const SnDev*, const double*, const int2*, int, const int2*, int, int, const double*,
+                           double*, double*);
+static int fw_variant() {
+  // swept on cfg3 (tools/slots_sweep.sh): 4 loads x 3 CTAs/SM, 4 x 148 slots
+  // 277 us; 8 x 2: 282 us; 12 x 2: 290 us; unbatched remainder loop: 288 us
+  static const int v = getenv("SPB_FW_VARIANT") ? atoi(getenv("SPB_FW_VARIANT")) : 0;
+  return v;
+}
+static FwLevelFn fw_level_kernel() {
+  switch (fw_variant()) {
+    case 0: return k_fw_level<4, 3>;
+    case 2: return k_fw_level<12, 2>;
+    default: return k_fw_level<8, 2>;
   }
 }
 
@@ -1370,7 +1401,8 @@ int build_device_factor(Factor& f) {
   if (!attr) {
     cudaFuncSetAttribute(k_forward_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
     cudaFuncSetAttribute(k_forward_flow, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
-    cudaFuncSetAttribute(k_fw_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
+    for (FwLevelFn fn : {k_fw_level<4, 3>, k_fw_level<8, 2>, k_fw_level<12, 2>})
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * CH_FW * 8 + 64);
     cudaFuncSetAttribute(k_bw_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 4096 * 8);
     attr = true;
   }
@@ -1430,7 +1462,7 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
                VZ);
     const int grid = T.ncta + (T.nwarp + FW_WARPS - 1) / FW_WARPS;
     const size_t smem = sizeof(double) * std::max(3 * std::min(T.max_nc, CH_FW), 3 * FW_THREADS);
-    launch_pdl(k_fw_level, dim3(grid), dim3(FW_THREADS), smem, st, (const SnDev*)d.sn, (const double*)d.M,
+    launch_pdl(fw_level_kernel(), dim3(grid), dim3(FW_THREADS), smem, st, (const SnDev*)d.sn, (const double*)d.M,
                (const int2*)(d.fw_cta + T.cta_off), T.ncta, (const int2*)(d.fw_warp + T.warp_off), T.nwarp,
                T.rows, (const double*)VZ, y, U);
     if (launches) *launches += 2;
