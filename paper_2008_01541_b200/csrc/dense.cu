@@ -372,15 +372,41 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
   const int tid = threadIdx.x, warp = tid >> 5;
   POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
+  // identity rows 64 + [r0, r0 + 16) of the inverse half (row 64 + i is first
+  // read by the panel solve of block i / 16: each block's rows are set while
+  // warp 0 factors the block before)
+  auto init_rows = [&](int r0, int t0, int nt) {
+    for (int q = t0; q < 16 * 64; q += nt) {
+      const int r = r0 + (q >> 6), c = q & 63;
+      S[(64 + r) * LSP + c] = (r == c) ? 1.0 : 0.0;
+    }
+  };
+  // columns [c0, c0 + 16) are final once their block's panel is solved:
+  // L_jj (lower) and L_jj^-T (upper; rows below the diagonal are zero and
+  // may not be initialized yet) go out while later blocks are factored
+  auto store_cols = [&](int c0, int t0, int nt, bool linv, bool l) {
+    for (int q = t0; q < 64 * 16; q += nt) {
+      const int r = q >> 4, c = c0 + (q & 15);
+      if (linv) {
+        const double v = (r <= c) ? S[(64 + r) * LSP + c] : 0.0;
+        gLinvT[swz(r, c)] = v;
+        if (MULTI)
+          for (int p = 0; p < pr.n; ++p) pr.LinvT[p][(size_t)j * TILE + swz(r, c)] = v;
+      }
+      if (l) {
+        const double v = (c <= r) ? S[r * LSP + c] : 0.0;
+        gL[swz(r, c)] = v;
+        if (MULTI)
+          for (int p = 0; p < pr.n; ++p) pr.L[p][(size_t)tidx(j, j) * TILE + swz(r, c)] = v;
+      }
+    }
+  };
   cons_sync();  // every warp has finished reading the stage area
   acc_foreach(wr, wc, lane, [&](int mb, int nb, int r, int c) {
     S[r * LSP + c] = acc.c[mb][nb][0];
     S[r * LSP + c + 1] = acc.c[mb][nb][1];
   });
-  for (int q = tid; q < 64 * 64; q += NCONS) {
-    const int r = q >> 6, c = q & 63;
-    S[(64 + r) * LSP + c] = (r == c) ? 1.0 : 0.0;
-  }
+  init_rows(0, tid, NCONS);
   cons_sync();
   POTRF_MARK(1)
 #pragma unroll 1
@@ -398,19 +424,40 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
         __syncwarp();
       }
       potrf_diag16(S, DT, o, j, info, lane);
-    } else if (kb > 0) {
-      const int rb0 = o >> 3, cb0 = rb0, nrb = 16 - rb0, ncb = 8 - cb0;
-      const int nblk = nrb * ncb;
+    } else {
+      if (kb < 3) init_rows(o + 16, tid - 32, NCONS - 32);
+      if (kb > 0) store_cols(o - 16, tid - 32, NCONS - 32, true, true);
+    }
+    if (warp > 0 && kb > 0) {
+      // only the 8x8 blocks the update changes, listed compactly: the lower
+      // blocks of A below warp 0's two block rows, then the rows of the
+      // inverse half that are nonzero in the panel (row 64 + i of [A; I]
+      // stays e_i in every column < i, so rows i >= o are still zero in
+      // panel columns [o - 16, o))
+      const int rb0 = o >> 3, cb0 = rb0, ncb = 8 - cb0;
+      int ntop = 0;
+      for (int rb = rb0 + 2; rb < 8; ++rb) ntop += rb - cb0 + 1;
+      const int nblk = ntop + (o >> 3) * ncb;
       for (int b2 = warp - 1; b2 < nblk; b2 += 2 * (NCONS / 32 - 1)) {
         int rbu[2], cbu[2];
         bool oku[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int bidx = b2 + u * (NCONS / 32 - 1);
-          rbu[u] = rb0 + bidx / ncb;
-          cbu[u] = cb0 + bidx % ncb;
-          const bool diag = rbu[u] < rb0 + 2 && cbu[u] < cb0 + 2;  // warp 0's
-          oku[u] = bidx < nblk && !diag && !(rbu[u] < 8 && rbu[u] < cbu[u]);  // unused upper blocks
+          int bidx = b2 + u * (NCONS / 32 - 1);
+          oku[u] = bidx < nblk;
+          if (bidx < ntop) {
+            int rb = rb0 + 2;
+            while (bidx >= rb - cb0 + 1) {
+              bidx -= rb - cb0 + 1;
+              ++rb;
+            }
+            rbu[u] = rb;
+            cbu[u] = cb0 + bidx;
+          } else {
+            bidx -= ntop;
+            rbu[u] = 8 + bidx / ncb;
+            cbu[u] = cb0 + bidx % ncb;
+          }
         }
         upd_block2(S, o - 16, rbu[0], cbu[0], oku[0], rbu[1], cbu[1], oku[1], g, t);
       }
@@ -418,8 +465,9 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
     cons_sync();
     POTRF_MARK(2 + 2 * kb)
     // (b) panel: rows [o+16, 128) x cols [o, o+16): P = S_panel * D^-T (in place)
-    const int pb0 = (o + 16) >> 3;
-    for (int rb = pb0 + warp; rb < 16; rb += NCONS / 32) {
+    // (rows 64 + i of the inverse half with i >= o + 16 are still zero here)
+    const int pb0 = (o + 16) >> 3, pb1 = min(16, 8 + ((o + 16) >> 3));
+    for (int rb = pb0 + warp; rb < pb1; rb += NCONS / 32) {
       double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
       const double* pa = S + (rb * 8 + g) * LSP + o + t;
 #pragma unroll
@@ -438,15 +486,9 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
     cons_sync();
     POTRF_MARK(3 + 2 * kb)
   }
-  // L_jj^-T first (the next tasks read only it: the kernel never reads the
-  // diagonal L tiles), publish, then L_jj (strict upper zeroed)
-  for (int q = tid; q < 64 * 64; q += NCONS) {
-    const int r = q >> 6, c = q & 63;
-    const double v = S[(64 + r) * LSP + c];
-    gLinvT[swz(r, c)] = v;
-    if (MULTI)
-      for (int p = 0; p < pr.n; ++p) pr.LinvT[p][(size_t)j * TILE + swz(r, c)] = v;
-  }
+  // the last columns of L_jj^-T (the next tasks read only it: the kernel
+  // never reads the diagonal L tiles), publish, then the last columns of L_jj
+  store_cols(48, tid, NCONS, true, false);
   if (flag) {
     fence_proxy_async_global();
     fence_tile_stores<MULTI>();
@@ -456,13 +498,7 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
       if (MULTI) release_peers(pr, tidx(j, j), 1);
     }
   }
-  for (int q = tid; q < 64 * 64; q += NCONS) {
-    const int r = q >> 6, c = q & 63;
-    const double v = (c <= r) ? S[r * LSP + c] : 0.0;
-    gL[swz(r, c)] = v;
-    if (MULTI)
-      for (int p = 0; p < pr.n; ++p) pr.L[p][(size_t)tidx(j, j) * TILE + swz(r, c)] = v;
-  }
+  store_cols(48, tid, NCONS, false, true);
   POTRF_MARK(14)
 }
 

@@ -20,7 +20,9 @@ __global__ void __launch_bounds__(288, 1) k_potrf_bench(const double* A, double*
     acc.c[mb][nb][1] = A[r * 64 + c + 1];
   });
   long long t0 = clock64();
-  for (int r = 0; r < reps; ++r) potrf_blocked_tile(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane);
+  const DensePeers nop{};
+  for (int r = 0; r < reps; ++r)
+    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop);
   long long t1 = clock64();
   // diag16 alone
   for (int r = 0; r < reps; ++r) {
