@@ -257,7 +257,8 @@ __device__ __forceinline__ void add_c22(const DenseDev& d, int tile, double* S) 
 // L_jj (lower), rows 64..127 as L_jj^-T (upper). 3 consumer barriers per
 // block instead of one per column.
 constexpr int LSP = 68;        // row stride of the augmented panel (bank slots (4g + t) mod 16)
-constexpr int LDT = 20;        // row stride of the 16 x 16 D^-T block
+constexpr int LDT = 20;
+constexpr int UPD_WARPS = NCONS / 32 - 1;  // consumer warps beside warp 0        // row stride of the 16 x 16 D^-T block
 
 // 1/sqrt(x) for the (positive, normal) pivots without the library's
 // special-case call path, whose ABI spills the live panel registers on every
@@ -271,6 +272,16 @@ __device__ __forceinline__ double pivot_rsqrt(double x) {
   const double e = fma(-(x * y), y, 1.0);
   const double p = fma(e, 0.375, 0.5);
   return fma(y * e, p, y);
+}
+
+// 1/x for the pivot chain: hardware approximation + one cubic correction,
+// y (1 + e + e^2) with e = 1 - x y (3 dependent FMAs)
+__device__ __forceinline__ double pivot_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y, 1.0);
+  const double t = fma(e, e, e);
+  return fma(y, t, y);
 }
 
 // double shuffle as two explicit 32-bit shuffles (the generic overload makes
@@ -295,16 +306,17 @@ __device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j
     badk = (badk < 0 && !(dkk > 0.0)) ? k : badk;
     const double ip = pivot_rsqrt(dkk);
     const bool active = lane > k;  // rows below the pivot (all identity lanes)
-    const double l = v[k] * ip;
+    const double u = v[k];
+    const double l = u * ip;
     // one select per column instead of one per updated entry: rows at or
     // above the pivot multiply by zero (their entries stay as they are)
     const double lm = active ? l : 0.0;
     v[k] = (lane == k) ? dkk * ip : (active ? l : v[k]);
     if (k < 15) {
-      // critical chain first: lane k+1's updated diagonal needs only its own
-      // l (v[k+1] - l^2, bitwise what the shuffled update gives it), so the
-      // next pivot is one shuffle away
-      dnext = shfl_f64(fma(-lm, l, v[k + 1]), k + 1);
+      // critical chain first: lane k+1's next pivot needs only its own
+      // entries, a_{k+1,k+1} - a_{k+1,k}^2 / d_k: the chain runs through one
+      // reciprocal (the column scaling's rsqrt is off it), then one shuffle
+      dnext = shfl_f64(fma(-(u * u), pivot_rcp(dkk), v[k + 1]), k + 1);
     }
     // broadcast the column through shared memory: one store per lane and one
     // broadcast load per entry instead of two 32-bit shuffles per entry
@@ -438,12 +450,12 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
       int ntop = 0;
       for (int rb = rb0 + 2; rb < 8; ++rb) ntop += rb - cb0 + 1;
       const int nblk = ntop + (o >> 3) * ncb;
-      for (int b2 = warp - 1; b2 < nblk; b2 += 2 * (NCONS / 32 - 1)) {
+      for (int b2 = warp - 1; b2 < nblk; b2 += 2 * UPD_WARPS) {
         int rbu[2], cbu[2];
         bool oku[2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          int bidx = b2 + u * (NCONS / 32 - 1);
+          int bidx = b2 + u * UPD_WARPS;
           oku[u] = bidx < nblk;
           if (bidx < ntop) {
             int rb = rb0 + 2;

@@ -1,6 +1,8 @@
 // Microbenchmark of the diagonal-tile factorization pieces (diagnostics).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2008_01541_b200/csrc potrf_bench.cu ...
+#ifndef NOPROF
 #define SPB_POTRF_PROF 1
+#endif
 #include "../paper_2008_01541_b200/csrc/dense.cu"
 
 namespace spb {
@@ -63,6 +65,7 @@ int main() {
   cudaMemcpy(&hi, info, 4, cudaMemcpyDeviceToHost);
   printf("err=%s info=%d potrf_blocked %lld cyc (%.2f us @1.9GHz), diag16 %lld cyc, cons_sync %lld cyc\n",
          cudaGetErrorString(cudaGetLastError()), hi, h[0], h[0] / 1900.0, h[1], h[2]);
+#ifndef NOPROF
   long long prof[32];
   cudaMemcpyFromSymbol(prof, g_potrf_prof, sizeof(prof));
   // phases are cumulative clocks over 20 reps (+ the diag16-only loop does not mark)
@@ -75,6 +78,7 @@ int main() {
     prev = prof[k];
   }
   printf("  %-10s %8.0f cyc\n", "store", (prof[14] - prev) / 20.0);
+#endif
   double hL[4096];
   cudaMemcpy(hL, L, 4096 * 8, cudaMemcpyDeviceToHost);
   // check L L^T == A
