@@ -374,13 +374,46 @@ __device__ __forceinline__ void upd_block2(double* S, int o, int rbA, int cbA, b
     }
 }
 
+// S[rb][cb] -= U[rb rows] U[cb rows]^T over K = 64 with U a swizzled 64x64
+// tile (the sub-diagonal L(j, j-1) of the diagonal task), two 8x8 blocks per
+// call; the k order and the DMMA accumulation are those of mma_abt<true>, so
+// the result is bitwise the register-tile update it replaces
+__device__ __forceinline__ void upd_block2_tile(double* S, const double* U, int rbA, int cbA, bool okA, int rbB,
+                                                int cbB, bool okB, int g, int t) {
+  const int rb[2] = {okA ? rbA : 0, okB ? rbB : 0}, cb[2] = {okA ? cbA : 0, okB ? cbB : 0};
+  const bool ok[2] = {okA, okB};
+  double c0[2], c1[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const double* pc = S + (rb[u] * 8 + g) * LSP + cb[u] * 8 + 2 * t;
+    c0[u] = ok[u] ? pc[0] : 0.0;
+    c1[u] = ok[u] ? pc[1] : 0.0;
+  }
+#pragma unroll
+  for (int k0 = 0; k0 < TS; k0 += 4)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      dmma(c0[u], c1[u], -U[swz(rb[u] * 8 + g, k0 + t)], U[swz(cb[u] * 8 + g, k0 + t)]);
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+    if (ok[u]) {
+      double* pc = S + (rb[u] * 8 + g) * LSP + cb[u] * 8 + 2 * t;
+      pc[0] = c0[u];
+      pc[1] = c1[u];
+    }
+}
+
 // Look-ahead blocked factorization: after the panel solve of column block kb,
 // warp 0 updates the next 16x16 diagonal block and factors it right away while
 // warps 1-7 apply the rest of the rank-16 trailing update, so the sequential
 // 16-pivot kernels overlap the update work (2 consumer barriers per block).
 template <bool MULTI>
+// upd (optional): a swizzled tile U whose rank-64 update A -= U U^T is still
+// due (the diagonal task's sub-diagonal tile): warp 0 applies it to the first
+// 16x16 block and starts factoring while warps 1-7 apply the rest.
 __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
-                                   int* info, int* flag, int wr, int wc, int lane, const DensePeers& pr) {
+                                   int* info, int* flag, int wr, int wc, int lane, const DensePeers& pr,
+                                   const double* upd) {
   const int tid = threadIdx.x, warp = tid >> 5;
   POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
@@ -428,6 +461,39 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
     // [o, 64)): warp 0 updates the 16x16 diagonal block of kb and factors it
     // right away (one call site: the unrolled 16-pivot kernel is large);
     // warps 1..7 update every other block meanwhile
+    if (kb == 0 && upd && warp < 4) {
+      // the first 16x16 block of A -= U U^T is on the chain: warps 0-3 (one
+      // per SM sub-partition) each take a quarter of K for its three 8x8
+      // blocks, warp 0 adds the quarters in fixed order
+      double* part = DT + 16 * LDT + 64;  // 4 x 3 x 64 doubles past the pivot buffers
+      double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const int brb[3] = {0, 1, 1}, bcb[3] = {0, 0, 1};
+#pragma unroll
+      for (int s4 = 0; s4 < 4; ++s4) {
+        const int k0 = 16 * warp + 4 * s4;
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          dmma(c[b][0], c[b][1], -upd[swz(brb[b] * 8 + g, k0 + t)], upd[swz(bcb[b] * 8 + g, k0 + t)]);
+      }
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        part[(warp * 3 + b) * 64 + g * 8 + 2 * t] = c[b][0];
+        part[(warp * 3 + b) * 64 + g * 8 + 2 * t + 1] = c[b][1];
+      }
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      if (warp == 0) {
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int q = g * 8 + 2 * t + e;
+            double* ps = S + (brb[b] * 8 + g) * LSP + bcb[b] * 8 + 2 * t + e;
+            *ps += (part[(0 * 3 + b) * 64 + q] + part[(1 * 3 + b) * 64 + q]) +
+                   (part[(2 * 3 + b) * 64 + q] + part[(3 * 3 + b) * 64 + q]);
+          }
+        __syncwarp();
+      }
+    }
     if (warp == 0) {
       if (kb > 0) {
         const int d0 = o >> 3;
@@ -437,6 +503,26 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
       }
       potrf_diag16(S, DT, o, j, info, lane);
     } else {
+      if (kb == 0 && upd) {
+        // the rest of A -= U U^T: lower 8x8 blocks of rows 16..63 (33 blocks)
+        constexpr int NB = 33;
+        for (int b2 = warp - 1; b2 < NB; b2 += 2 * UPD_WARPS) {
+          int rbu[2], cbu[2];
+          bool oku[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            int bidx = b2 + u * UPD_WARPS, rb = 2;
+            oku[u] = bidx < NB;
+            while (oku[u] && bidx > rb) {
+              bidx -= rb + 1;
+              ++rb;
+            }
+            rbu[u] = rb;
+            cbu[u] = oku[u] ? bidx : 0;
+          }
+          upd_block2_tile(S, upd, rbu[0], cbu[0], oku[0], rbu[1], cbu[1], oku[1], g, t);
+        }
+      }
       if (kb < 3) init_rows(o + 16, tid - 32, NCONS - 32);
       if (kb > 0) store_cols(o - 16, tid - 32, NCONS - 32, true, true);
     }
@@ -674,9 +760,9 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       if (MULTI)
         for (int p = 0; p < d.peers.n; ++p)
           acc_to_swz(out, d.peers.L[p] + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
-      cons_sync();
-      mma_abt<true>(acc, scratch, scratch, wr, wc, lane);  // its rank-64 update first ...
-      fence_proxy_async_global();                          // ... then publish (the fence overlapped it)
+      // its rank-64 update A -= L(j, j-1) L(j, j-1)^T is applied inside the
+      // factorization (from the scratch copy), off the chain but its first block
+      fence_proxy_async_global();
       fence_tile_stores<MULTI>();
       cons_sync();
       if (tid == 0) {
@@ -693,7 +779,8 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
     if (i == j) {
       // the producer is parked: the whole stage area holds the augmented panel + D^-T
       potrf_blocked_tile<MULTI>(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
-                                d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane, d.peers);
+                                d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane, d.peers,
+                                j > 0 ? sm.scratch : nullptr);
     } else if (i == j + 1 && !rhs) {
       // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
       acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(288, 1) k_potrf_bench(const double* A, double*
   long long t0 = clock64();
   const DensePeers nop{};
   for (int r = 0; r < reps; ++r)
-    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop);
+    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop, nullptr);
   long long t1 = clock64();
   // diag16 alone
   for (int r = 0; r < reps; ++r) {
