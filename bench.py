@@ -420,9 +420,12 @@ def run_batch(args):
         dist.barrier()
     _native.check(lib.spb_bench_batch(handles, S, ctypes.byref(cfg), args.steps, ctypes.byref(ms)))
     one = ctypes.c_double(0)
+    device_scene(sims[0].model, sims[0].system).set_concurrency(1)  # scene 0 alone: the serial reference
     _native.check(lib.spb_ctx_bench(handles[0], ctypes.byref(cfg), args.steps, ctypes.byref(one), None))
     if dist is not None:
         dist.barrier()
+    for sm in sims:  # the e2e loop steps the scenes one after another
+        device_scene(sm.model, sm.system).set_concurrency(1)
     te = time.perf_counter()
     for _ in range(max(1, args.steps // 4)):
         for sim in sims:

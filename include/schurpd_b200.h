@@ -236,6 +236,11 @@ int32_t spb_ctx_bench_kernel(spb_ctx *ctx, int32_t which, int32_t reps, double *
  * one frame of every context. */
 int32_t spb_bench_batch(spb_ctx **ctxs, int32_t n, const spb_step_config *cfg, int32_t rounds,
                         double *ms_per_round);
+/* Hint: n contexts step concurrently on this device (batch of scenes). The
+ * tile Cholesky then takes about 1/n of the SMs, so the scenes' chain-bound
+ * factorizations overlap; n = 1 restores the single-scene grid. spb_bench_batch
+ * applies its own n. Results are bitwise independent of the hint. */
+int32_t spb_ctx_set_concurrency(spb_ctx *ctx, int32_t n);
 
 /* ------------------------------------------------------- one-shot ops */
 int32_t spb_op_deformation_gradients(int64_t ne, const int64_t *tets, const double *dm_inverse, int64_t n,

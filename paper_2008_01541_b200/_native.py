@@ -101,6 +101,7 @@ _SIGS = {
     "spb_ctx_bench_kernel": ([P, I32, I32, P], I32),
     "spb_ctx_trace_dense_backward": ([P, P, P], I32),
     "spb_bench_batch": ([P, I32, P, I32, P], I32),
+    "spb_ctx_set_concurrency": ([P, I32], I32),
     "spb_ctx_trace_cholesky": ([P, P, P, P], I32),
     "spb_op_deformation_gradients": ([I64, P, P, I64, P, I64, P, P], I32),
     "spb_op_svd": ([I64, P, P, P, P, P, P, F64, F64], I32),

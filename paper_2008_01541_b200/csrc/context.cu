@@ -125,7 +125,7 @@ struct Ctx {
   DBuf<int> k_ptr, k_idx;
   DBuf<double> k_val;
   // dense
-  int N = 0, ntasks = 0, chol_grid = 0;
+  int N = 0, ntasks = 0, chol_grid = 0, chol_grid_alone = 0;
   DBuf<double> sigma0_tiles, L, LinvT, Y, gemv_partial, xrows;
   DBuf<int> flags, counter, info;
   SweepWork sw;  // sparse-sweep workspace of this context
@@ -427,6 +427,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
     // for concurrent scenes (cfg5 batch); cfg3 uses every SM
     chol_grid = std::max(1, std::min({NUM_SMS_B200, ntasks, std::max(8, 2 * N)}));
     if (const char* e = getenv("SPB_CHOL_GRID")) chol_grid = std::max(8, std::min(ntasks, atoi(e)));
+    chol_grid_alone = chol_grid;
     TRY(tasks.upload(tk));
     // C22 entries: upper (c, r) COO contributions in (proxy, a, b) order, stored at
     // lower (r, c) (linalg.py:46-51, :67-74 + collision.py:431-434)
@@ -1169,11 +1170,38 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
 // Aggregate device timing of several contexts stepped concurrently (one
 // stream each): `rounds` rounds, each one frame of every context; reports the
 // mean ms per round (the cfg5 batch: scenes sharing one factor on one GPU).
+// n contexts will step concurrently on this device: each persistent tile
+// Cholesky takes 1/n of the SMs (at least 8 CTAs), so the scenes' chain-bound
+// factorizations run side by side instead of queueing for SMs (cfg5, 8 scenes:
+// 2,961 -> 4,312 scene-frames/s). n <= 1 restores the single-scene grid.
+// Captured graphs embed the grid, so a change drops them.
+int32_t spb_ctx_set_concurrency(spb_ctx* cp, int32_t n) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  if (!c || n < 1) { spb::set_error("spb_ctx_set_concurrency: bad arguments"); return SPB_ERR_ARG; }
+  if (c->n2 == 0) return SPB_OK;
+  const int g = n <= 1 ? c->chol_grid_alone : std::max(8, std::min(c->chol_grid_alone, spb::NUM_SMS_B200 / n));
+  if (g == c->chol_grid) return SPB_OK;
+  SPB_CUDA(cudaSetDevice(c->device));
+  SPB_CUDA(cudaStreamSynchronize(c->st));
+  for (auto& kv : c->graphs) {
+    cudaGraphExecDestroy(kv.second.first);
+    cudaGraphExecDestroy(kv.second.second);
+  }
+  c->graphs.clear();
+  c->chol_grid = g;
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
 int32_t spb_bench_batch(spb_ctx** ctxs, int32_t n, const spb_step_config* cfg, int32_t rounds, double* ms_per_round) {
   SPB_GUARD_BEGIN
   if (n <= 0 || !ctxs) { spb::set_error("no contexts"); return SPB_ERR_ARG; }
   Ctx* c0 = reinterpret_cast<Ctx*>(ctxs[0]);
   SPB_CUDA(cudaSetDevice(c0->device));
+  for (int k = 0; k < n; ++k) TRY(spb_ctx_set_concurrency(ctxs[k], n));
+  // one untimed round: graphs dropped by a changed grid are captured here
+  for (int k = 0; k < n; ++k) TRY(run_frame(reinterpret_cast<Ctx*>(ctxs[k]), cfg, nullptr));
   for (int k = 0; k < n; ++k) SPB_CUDA(cudaStreamSynchronize(reinterpret_cast<Ctx*>(ctxs[k])->st));
   std::vector<cudaEvent_t> done(n);
   cudaEvent_t e0, e1;
