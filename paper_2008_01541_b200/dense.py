@@ -109,8 +109,13 @@ class DenseCholesky:
         nat.check(nat.lib().spb_dense_get_matrix(self._h, nat.ptr(out)))
         return out
 
-    def factor_lower(self, replica: int = 0) -> np.ndarray:
-        out = np.zeros((self.m, self.m))
+    def factor_lower(self, replica: int = 0, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """L (row-major, strict upper zero), into `out` when given (a reused,
+        page-locked buffer makes the download one direct DMA)."""
+        if out is None:
+            out = np.empty((self.m, self.m))
+        elif out.shape != (self.m, self.m) or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise InvalidArgumentError("out must be a C-contiguous float64 m x m array")
         nat.check(nat.lib().spb_dense_get_factor(self._h, replica, nat.ptr(out)))
         return out
 
