@@ -126,6 +126,7 @@ struct Ctx {
   DBuf<double> k_val;
   // dense
   int N = 0, ntasks = 0, chol_grid = 0, chol_grid_alone = 0;
+  bool aux_overlap = true;  // second-stream overlap of the last inner pass (off for concurrent scenes)
   DBuf<double> sigma0_tiles, L, LinvT, Y, gemv_partial, xrows;
   DBuf<int> flags, counter, info;
   SweepWork sw;  // sparse-sweep workspace of this context
@@ -143,6 +144,8 @@ struct Ctx {
   char* io_host = nullptr;           // pinned staging for set_state / get_state
   size_t io_bytes = 0;
   cudaStream_t st_io = nullptr;      // state download overlapping the metrics kernels
+  cudaStream_t st_aux = nullptr;     // sigma0 u2 + f~2 upkeep beside the backward sweep (last inner pass)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_state = nullptr;    // recorded between the solve and the metrics: the state is final
   // metrics
   DBuf<double> e_part, a_part, p_part, r_part, metrics_out;
@@ -180,6 +183,9 @@ struct Ctx {
     if (pcg_resid_host) cudaFreeHost(pcg_resid_host);
     if (ev_state) cudaEventDestroy(ev_state);
     if (st_io) cudaStreamDestroy(st_io);
+    if (st_aux) cudaStreamDestroy(st_aux);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -275,6 +281,9 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   SPB_CUDA(cudaSetDevice(device));
   SPB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   SPB_CUDA(cudaStreamCreateWithFlags(&st_io, cudaStreamNonBlocking));
+  SPB_CUDA(cudaStreamCreateWithFlags(&st_aux, cudaStreamNonBlocking));
+  SPB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+  SPB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
   SPB_CUDA(cudaEventCreateWithFlags(&ev_state, cudaEventDisableTiming));
   factor = f;
   n = s->num_nodes;
@@ -491,6 +500,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
   int launches = 0;
   const ProxyDev P_ = px();
   bool first_detection_done = false;
+  bool aux_pending = false;
   residual_valid = false;
   if (ev) SPB_CUDA(cudaEventRecord(ev[0], st));
   for (int o = 0; o < outer; ++o) {
@@ -526,24 +536,43 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
       launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid);
       launch_dense_backward(st, dd, xrows.p, u2.p);
-      // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual
-      launch_sym_tile_gemv(st, dd, u2.p, gemv_partial.p);
-      launch_sym_tile_gemv_reduce(st, dd, gemv_partial.p, s0u.p);
-      launch_proxy_wu(st, P_, active.p, u2.p, vprox.p);
-      launch_inner_update(st, n2, u2.p, s0u.p, k_ptr.p, k_idx.p, k_val.p, g.p, prox_w.p, vprox.p, gc_ptr.p,
-                          gc_src.p, f_tilde2.p, u2acc.p, x.p, x2_ids.p, r_part.p);
+      // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual.
+      // In the last pass nothing downstream of the backward sweep needs f~2:
+      // u2_accum is updated on the main stream (it feeds the sweep) and the
+      // mat-vec + upkeep run on the aux stream beside the sweep (joined below)
+      cudaStream_t su = st;
+      static const bool aux_on = !(getenv("SPB_AUX_OVERLAP") && getenv("SPB_AUX_OVERLAP")[0] == '0');
+      const bool overlap = aux_on && aux_overlap && it == inner - 1 && n1 > 0;
+      if (overlap) {
+        launch_u2acc_to_xf(st, n2, u2.p, u2acc.p, XF.p + 3 * (size_t)n1);
+        SPB_CUDA(cudaEventRecord(ev_fork, st));
+        SPB_CUDA(cudaStreamWaitEvent(st_aux, ev_fork, 0));
+        su = st_aux;
+        launches++;
+      }
+      launch_sym_tile_gemv(su, dd, u2.p, gemv_partial.p);
+      launch_sym_tile_gemv_reduce(su, dd, gemv_partial.p, s0u.p);
+      launch_proxy_wu(su, P_, active.p, u2.p, vprox.p);
+      launch_inner_update(su, n2, u2.p, s0u.p, k_ptr.p, k_idx.p, k_val.p, g.p, prox_w.p, vprox.p, gc_ptr.p,
+                          gc_src.p, f_tilde2.p, overlap ? nullptr : u2acc.p, x.p, x2_ids.p, r_part.p);
+      if (overlap) SPB_CUDA(cudaEventRecord(ev_join, st_aux));
+      aux_pending = overlap;
       launches += (nbeta > 0) + 7 + (P > 0);
       residual_valid = true;
     }
     if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[3], st));
     // (5) u1 = L1^-T (y1 - C^T u2_accum); x1 += u1
     if (n1 > 0) {
-      if (n2 > 0)
+      if (n2 > 0 && !aux_pending)
         SPB_CUDA(cudaMemcpyAsync(XF.p + 3 * (size_t)n1, u2acc.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice,
                                  st));
       sparse_backward(st, *factor->dev, y.p, XF.p, &launches, &sw);
       launch_scatter_add(st, n1, x1_node.p, XF.p, x.p);
       launches++;
+    }
+    if (aux_pending) {
+      SPB_CUDA(cudaStreamWaitEvent(st, ev_join, 0));  // x2, f~2, residual partials
+      aux_pending = false;
     }
     if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[4], st));
   }
@@ -880,13 +909,15 @@ int32_t spb_ctx_get_state(spb_ctx* cp, double* x, double* R, double* Q, uint8_t*
 // One frame on the context stream. Between the solve and the metrics the
 // host records ev_state (the state is final), so a download on the io stream
 // can overlap the metrics kernels with plain stream-order semantics.
-static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
+// The (solve, metrics) graph pair of a step configuration, captured (not run)
+// on first use.
+static int ensure_graphs(Ctx* c, const spb_step_config* cfg,
+                         std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>::iterator* out) {
   const int outer = cfg->outer_iters, inner = cfg->inner_iters, cad = cfg->cadence;
-  TRY(c->sync_shapes());
-  if (cfg->use_graph && !ev) {
-    auto key = std::make_tuple(outer, inner, cad);
-    auto it = c->graphs.find(key);
-    if (it == c->graphs.end()) {
+  auto key = std::make_tuple(outer, inner, cad);
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    {
       cudaGraphExec_t exe[2];
       for (int part = 0; part < 2; ++part) {
         cudaGraph_t gph;
@@ -896,10 +927,22 @@ static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
         if (rc != SPB_OK) return rc;
         if (e2 != cudaSuccess) { spb::set_error(std::string("graph capture: ") + cudaGetErrorString(e2)); return SPB_ERR_CUDA; }
         SPB_CUDA(cudaGraphInstantiate(&exe[part], gph, 0));
+        SPB_CUDA(cudaGraphUpload(exe[part], c->st));  // the first launch pays no upload
         cudaGraphDestroy(gph);
       }
       it = c->graphs.emplace(key, std::make_pair(exe[0], exe[1])).first;
     }
+  }
+  if (out) *out = it;
+  return SPB_OK;
+}
+
+static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
+  const int outer = cfg->outer_iters, inner = cfg->inner_iters, cad = cfg->cadence;
+  TRY(c->sync_shapes());
+  if (cfg->use_graph && !ev) {
+    std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>::iterator it;
+    TRY(ensure_graphs(c, cfg, &it));
     SPB_CUDA(cudaGraphLaunch(it->second.first, c->st));
     SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
     SPB_CUDA(cudaGraphLaunch(it->second.second, c->st));
@@ -1173,15 +1216,19 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
 // n contexts will step concurrently on this device: each persistent tile
 // Cholesky takes 1/n of the SMs (at least 8 CTAs), so the scenes' chain-bound
 // factorizations run side by side instead of queueing for SMs (cfg5, 8 scenes:
-// 2,961 -> 4,312 scene-frames/s). n <= 1 restores the single-scene grid.
-// Captured graphs embed the grid, so a change drops them.
+// 2,961 -> 4,312 scene-frames/s), and the frame keeps to one stream. n <= 1
+// restores the single-scene grid and the aux-stream overlap. Captured graphs
+// embed both, so a change drops them.
 int32_t spb_ctx_set_concurrency(spb_ctx* cp, int32_t n) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);
   if (!c || n < 1) { spb::set_error("spb_ctx_set_concurrency: bad arguments"); return SPB_ERR_ARG; }
   if (c->n2 == 0) return SPB_OK;
   const int g = n <= 1 ? c->chol_grid_alone : std::max(8, std::min(c->chol_grid_alone, spb::NUM_SMS_B200 / n));
-  if (g == c->chol_grid) return SPB_OK;
+  // concurrent scenes already fill the GPU, and a second stream per scene
+  // would exceed the device's hardware queues (false serialization)
+  const bool aux = n <= 1;
+  if (g == c->chol_grid && aux == c->aux_overlap) return SPB_OK;
   SPB_CUDA(cudaSetDevice(c->device));
   SPB_CUDA(cudaStreamSynchronize(c->st));
   for (auto& kv : c->graphs) {
@@ -1190,6 +1237,7 @@ int32_t spb_ctx_set_concurrency(spb_ctx* cp, int32_t n) {
   }
   c->graphs.clear();
   c->chol_grid = g;
+  c->aux_overlap = aux;
   return SPB_OK;
   SPB_GUARD_END
 }
@@ -1200,8 +1248,14 @@ int32_t spb_bench_batch(spb_ctx** ctxs, int32_t n, const spb_step_config* cfg, i
   Ctx* c0 = reinterpret_cast<Ctx*>(ctxs[0]);
   SPB_CUDA(cudaSetDevice(c0->device));
   for (int k = 0; k < n; ++k) TRY(spb_ctx_set_concurrency(ctxs[k], n));
-  // one untimed round: graphs dropped by a changed grid are captured here
-  for (int k = 0; k < n; ++k) TRY(run_frame(reinterpret_cast<Ctx*>(ctxs[k]), cfg, nullptr));
+  // graphs dropped by a changed grid are captured here, outside the timed
+  // region (captured only: the scenes' states do not advance)
+  if (cfg->use_graph)
+    for (int k = 0; k < n; ++k) {
+      Ctx* c = reinterpret_cast<Ctx*>(ctxs[k]);
+      TRY(c->sync_shapes());
+      TRY(ensure_graphs(c, cfg, nullptr));
+    }
   for (int k = 0; k < n; ++k) SPB_CUDA(cudaStreamSynchronize(reinterpret_cast<Ctx*>(ctxs[k])->st));
   std::vector<cudaEvent_t> done(n);
   cudaEvent_t e0, e1;

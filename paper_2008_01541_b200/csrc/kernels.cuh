@@ -146,6 +146,7 @@ void launch_inner_update(cudaStream_t st, int m, const double* u2, const double*
                          const int* cptr, const int* csrc, double* f_tilde2, double* u2acc, double* x,
                          const int* x2_ids, double* rpartial);
 void launch_scatter_add(cudaStream_t st, int cnt, const int* node, const double* X, double* x);
+void launch_u2acc_to_xf(cudaStream_t st, int m, const double* u2, double* u2acc, double* xf2);
 void launch_gather3(cudaStream_t st, int cnt, const int* idx, const double* src, double* out);
 int attachment_blocks(int na);
 void launch_attachment_energy(cudaStream_t st, int na, const int* nodes, const double* k, const double* tgt,

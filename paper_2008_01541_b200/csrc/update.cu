@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k_inner_update(int m, const double* __res
       gg += g[3 * k + q] * g[3 * k + q];
       x[3 * node + q] += u;
       f_tilde2[3 * k + q] -= s - ku[q];
-      u2acc[3 * k + q] += u;
+      if (u2acc) u2acc[3 * k + q] += u;  // null: k_u2acc_to_xf already did it
     }
   }
   rr = warp_sum(rr);
@@ -185,6 +185,23 @@ void launch_inner_update(cudaStream_t st, int m, const double* u2, const double*
   if (m <= 0) return;
   k_inner_update<<<update_blocks(m), 256, 0, st>>>(m, u2, s0u, kptr, kidx, kval, g, pw, v, cptr, csrc, f_tilde2,
                                                    u2acc, x, x2_ids, rpartial);
+}
+
+// The last inner pass's u2_accum upkeep, split off k_inner_update so the
+// backward sweep can start while the sigma0 mat-vec and the f~2 upkeep run on
+// a second stream: u2acc += u2 (the same single add), XF's x2 rows = u2acc.
+__global__ void k_u2acc_to_xf(int m3, const double* __restrict__ u2, double* __restrict__ u2acc,
+                              double* __restrict__ xf2) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m3) return;
+  const double v = u2acc[k] + u2[k];
+  u2acc[k] = v;
+  xf2[k] = v;
+}
+
+void launch_u2acc_to_xf(cudaStream_t st, int m, const double* u2, double* u2acc, double* xf2) {
+  if (m <= 0) return;
+  k_u2acc_to_xf<<<ceil_div(3 * (int64_t)m, 256), 256, 0, st>>>(3 * m, u2, u2acc, xf2);
 }
 
 void launch_scatter_add(cudaStream_t st, int cnt, const int* node, const double* X, double* x) {
