@@ -145,7 +145,7 @@ struct Ctx {
   size_t io_bytes = 0;
   cudaStream_t st_io = nullptr;      // state download overlapping the metrics kernels
   cudaStream_t st_aux = nullptr;     // sigma0 u2 + f~2 upkeep beside the backward sweep (last inner pass)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork0 = nullptr, ev_pre = nullptr;
   cudaEvent_t ev_state = nullptr;    // recorded between the solve and the metrics: the state is final
   // metrics
   DBuf<double> e_part, a_part, p_part, r_part, metrics_out;
@@ -186,6 +186,8 @@ struct Ctx {
     if (st_aux) cudaStreamDestroy(st_aux);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_fork0) cudaEventDestroy(ev_fork0);
+    if (ev_pre) cudaEventDestroy(ev_pre);
     if (st) cudaStreamDestroy(st);
   }
 
@@ -284,6 +286,8 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   SPB_CUDA(cudaStreamCreateWithFlags(&st_aux, cudaStreamNonBlocking));
   SPB_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
   SPB_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  SPB_CUDA(cudaEventCreateWithFlags(&ev_fork0, cudaEventDisableTiming));
+  SPB_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
   SPB_CUDA(cudaEventCreateWithFlags(&ev_state, cudaEventDisableTiming));
   factor = f;
   n = s->num_nodes;
@@ -503,7 +507,23 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
   bool aux_pending = false;
   residual_valid = false;
   if (ev) SPB_CUDA(cudaEventRecord(ev[0], st));
+  static const bool aux_on = !(getenv("SPB_AUX_OVERLAP") && getenv("SPB_AUX_OVERLAP")[0] == '0');
   for (int o = 0; o < outer; ++o) {
+    // The first inner pass's detection and beta local step read only x,
+    // which neither the alpha step nor the forward sweep changes: they run on
+    // the aux stream beside them and are joined before g is built
+    const bool pre = aux_on && aux_overlap && n2 > 0 && !ev;
+    if (pre) {
+      SPB_CUDA(cudaEventRecord(ev_fork0, st));
+      SPB_CUDA(cudaStreamWaitEvent(st_aux, ev_fork0, 0));
+      const bool fresh0 = cadence == SPB_CADENCE_INNER || (cadence == SPB_CADENCE_FRAME && !first_detection_done);
+      if (fresh0 && P > 0) {
+        launch_detect(st_aux, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
+        launches++;
+      }
+      launch_local_forces(st_aux, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
+      SPB_CUDA(cudaEventRecord(ev_pre, st_aux));
+    }
     // (1) local step on E_alpha fused with (2) the alpha element forces
     launch_local_forces(st, nalpha, e_alpha.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Ga.p, 1);
     launch_gather_forces(st, (int)n, ga_ptr.p, ga_src.p, Ga.p, nalpha, fac_node.p, att_ptr.p, att_idx.p, att_k.p,
@@ -520,14 +540,19 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
     if (ev && o == outer - 1) SPB_CUDA(cudaEventRecord(ev[2], st));
     for (int it = 0; it < inner; ++it) {
       bool fresh = cadence == SPB_CADENCE_INNER || (cadence == SPB_CADENCE_FRAME && !first_detection_done);
-      if (fresh && P > 0) {
-        launch_detect(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
-        launches++;
+      if (pre && it == 0) {
+        SPB_CUDA(cudaStreamWaitEvent(st, ev_pre, 0));  // detection + beta step done on the aux stream
+        first_detection_done = true;
+      } else {
+        if (fresh && P > 0) {
+          launch_detect(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
+          launches++;
+        }
+        first_detection_done = true;
+        if (n2 == 0) continue;
+        // (4.2) local step on E_beta fused with the beta element forces
+        launch_local_forces(st, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
       }
-      first_detection_done = true;
-      if (n2 == 0) continue;
-      // (4.2) local step on E_beta fused with the beta element forces
-      launch_local_forces(st, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
       // (4.4) g = f~2 + f_beta + f_col, packed as the RHS tile row
       launch_build_g(st, n2, f_tilde2.p, gb_ptr.p, gb_src.p, Gb.p, nbeta, P_, tets.p, x.p, active.p, target.p,
                      gc_ptr.p, gc_src.p, g.p, Y.p);
@@ -541,7 +566,6 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       // u2_accum is updated on the main stream (it feeds the sweep) and the
       // mat-vec + upkeep run on the aux stream beside the sweep (joined below)
       cudaStream_t su = st;
-      static const bool aux_on = !(getenv("SPB_AUX_OVERLAP") && getenv("SPB_AUX_OVERLAP")[0] == '0');
       const bool overlap = aux_on && aux_overlap && it == inner - 1 && n1 > 0;
       if (overlap) {
         launch_u2acc_to_xf(st, n2, u2.p, u2acc.p, XF.p + 3 * (size_t)n1);
