@@ -140,6 +140,15 @@ def fill_ordering(pattern, coords: Optional[np.ndarray] = None) -> np.ndarray:
     perm = _native.fill_ordering(n, up, coords)
     if len(perm) != n or not np.array_equal(np.bincount(perm, minlength=n), np.ones(n, dtype=np.int64)):
         raise RuntimeError("fill ordering produced a non-bijective permutation")
+    # nested dissection targets meshes; on band-like graphs (a chain) its
+    # separators add fill the natural order avoids: keep whichever fills less
+    # (symbolic counts only, no factorization)
+    if n > 1:
+        full = (up + sp.triu(up, 1).T).tocsr()
+        nd = _native.symbolic_nnz(n, sp.triu(full[perm][:, perm], format="csc"))
+        nat = _native.symbolic_nnz(n, up)
+        if nat <= nd:
+            return np.arange(n, dtype=np.int64)
     return perm
 
 

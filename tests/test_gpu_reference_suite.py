@@ -1,0 +1,43 @@
+"""The REFERENCE's own test suite (138 tests of /root/reference/pkg/tests)
+run against this package through a `schurpd` module alias
+(tools/reference_suite.py). The copy lives in baseline/_ref/tests
+(git-ignored, like the rest of baseline/_ref); without it this test skips.
+
+Deselected, with the reason:
+  * test_harness.py::test_cli_* (3): the reference CLI is out of scope;
+  * test_solver.py::test_inner_loop_keeps_x1_bitwise_frozen,
+    ::test_early_exit_skips_remaining_outer_passes: they spy on the Python
+    function collision.detect being called per pass; detection runs inside the
+    device frame here. Their invariants (x1 frozen across inner passes, the
+    early exit) are checked on the device by tests/test_gpu_parity.py.
+Everything else must pass (133 tests, incl. acceptance criteria 1-9)."""
+
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+SUITE = ROOT / "baseline" / "_ref" / "tests"
+
+DESELECT = [
+    "test_harness.py::test_cli_run_and_errors",
+    "test_harness.py::test_cli_compare",
+    "test_harness.py::test_cli_solver_and_iteration_overrides",
+    "test_solver.py::test_inner_loop_keeps_x1_bitwise_frozen",
+    "test_solver.py::test_early_exit_skips_remaining_outer_passes",
+]
+
+
+@pytest.mark.skipif(not SUITE.exists(), reason="baseline/_ref/tests not present (cp -r /root/reference/pkg/tests)")
+def test_reference_suite_passes():
+    args = [sys.executable, str(ROOT / "tools" / "reference_suite.py"), "-q", "-p", "no:randomly"]
+    for d in DESELECT:
+        args += ["--deselect", str(SUITE / d)]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=1500)
+    tail = "\n".join(r.stdout.splitlines()[-15:])
+    assert r.returncode == 0, tail
+    assert " passed" in tail and "failed" not in tail, tail

@@ -1,0 +1,38 @@
+"""Run the REFERENCE's own test suite against this package:
+`schurpd` and its submodules are aliased to paper_2008_01541_b200, then
+pytest collects baseline/_ref/tests (a copy of /root/reference/pkg/tests,
+git-ignored like the rest of baseline/_ref, shipped to the GPU box).
+
+  python tools/reference_suite.py [pytest args]"""
+import importlib
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import paper_2008_01541_b200 as P  # noqa: E402
+
+sys.modules["schurpd"] = P
+for sub in ("collision", "errors", "harness", "linalg", "material", "mesh", "partition", "solver"):
+    sys.modules[f"schurpd.{sub}"] = importlib.import_module(f"paper_2008_01541_b200.{sub}")
+
+# the reference CLI (cli.py) is out of scope (tier framing): its tests fail,
+# the rest of test_harness.py still runs
+import types  # noqa: E402
+
+_cli = types.ModuleType("schurpd.cli")
+
+
+def _no_cli(*a, **k):
+    raise NotImplementedError("the reference CLI is out of scope for this package")
+
+
+_cli.main = _no_cli
+sys.modules["schurpd.cli"] = _cli
+
+import pytest  # noqa: E402
+
+tests = ROOT / "baseline" / "_ref" / "tests"
+if not tests.exists():
+    sys.exit("baseline/_ref/tests missing: cp -r /root/reference/pkg/tests baseline/_ref/tests")
+sys.exit(pytest.main([str(tests), "-p", "no:cacheprovider", "--rootdir", str(tests), *sys.argv[1:]]))
