@@ -544,28 +544,23 @@ int32_t spb_dense_residual(spb_dense* d, int32_t replica, const double* v, doubl
   const size_t n = (size_t)d->N * 64;
   std::vector<double> hv(n, 0.0), a(n), b(n);
   std::copy(v, v + d->m, hv.begin());
-  double *x = nullptr, *y = nullptr, *w = nullptr, *z = nullptr;
-  SPB_CUDA(cudaMalloc(&x, 4 * n * sizeof(double)));
-  y = x + n;
-  w = y + n;
-  z = w + n;
-  int st = SPB_OK;
-  do {
-    if (cudaMemcpy(x, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) break;
-    const double* L = d->reps[replica].L(d->lo);
-    spb::k_tile_matvec<<<d->N, 256, 0, d->st>>>(d->sigma0, d->N, 0, x, y);  // A v
-    spb::k_tile_matvec<<<d->N, 256, 0, d->st>>>(L, d->N, 2, x, w);          // L^T v
-    spb::k_tile_matvec<<<d->N, 256, 0, d->st>>>(L, d->N, 1, w, z);          // L L^T v
-    if (cudaStreamSynchronize(d->st) != cudaSuccess) break;
-    cudaMemcpy(a.data(), y, n * sizeof(double), cudaMemcpyDeviceToHost);
-    cudaMemcpy(b.data(), z, n * sizeof(double), cudaMemcpyDeviceToHost);
-  } while (0);
-  cudaError_t e = cudaGetLastError();
-  cudaFree(x);
-  if (e != cudaSuccess) {
-    spb::set_error(std::string("spb_dense_residual: ") + cudaGetErrorString(e));
-    return SPB_ERR_CUDA;
-  }
+  struct Buf {  // x | A v | L^T v | L L^T v
+    double* p = nullptr;
+    ~Buf() {
+      if (p) cudaFree(p);
+    }
+  } buf;
+  SPB_CUDA(cudaMalloc(&buf.p, 4 * n * sizeof(double)));
+  double *x = buf.p, *y = x + n, *w = y + n, *z = w + n;
+  SPB_CUDA(cudaMemcpy(x, hv.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  const double* L = d->reps[replica].L(d->lo);
+  spb::k_tile_matvec<<<d->N, 256, 0, d->st>>>(d->sigma0, d->N, 0, x, y);  // A v
+  spb::k_tile_matvec<<<d->N, 256, 0, d->st>>>(L, d->N, 2, x, w);          // L^T v
+  spb::k_tile_matvec<<<d->N, 256, 0, d->st>>>(L, d->N, 1, w, z);          // L L^T v
+  SPB_CUDA(cudaGetLastError());
+  SPB_CUDA(cudaStreamSynchronize(d->st));
+  SPB_CUDA(cudaMemcpy(a.data(), y, n * sizeof(double), cudaMemcpyDeviceToHost));
+  SPB_CUDA(cudaMemcpy(b.data(), z, n * sizeof(double), cudaMemcpyDeviceToHost));
   double rr = 0.0, aa = 0.0;
   for (int64_t k = 0; k < d->m; ++k) {
     rr += (a[k] - b[k]) * (a[k] - b[k]);
@@ -573,7 +568,7 @@ int32_t spb_dense_residual(spb_dense* d, int32_t replica, const double* v, doubl
   }
   out2[0] = std::sqrt(rr);
   out2[1] = std::sqrt(aa);
-  return st;
+  return SPB_OK;
   SPB_GUARD_END
 }
 
