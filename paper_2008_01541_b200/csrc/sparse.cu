@@ -1236,7 +1236,8 @@ int build_device_factor(Factor& f) {
   d->bww_off[f.nlevels] = (int)bww.size();
   // ---- bottom subtrees: choose the fuse height f by a small cost model
   // (slowest group's panel bytes at ~25 GB/s effective per SM + ~20 us per remaining
-  // level launch pair), group whole subtrees (LPT on bytes, 148 groups)
+  // level launch pair + ~8 us per fused level), group whole subtrees (LPT on
+  // bytes, 148 groups)
   {
     std::vector<std::vector<int64_t>> kids(ns);
     for (int64_t s = 0; s < ns; ++s)
@@ -1271,7 +1272,10 @@ int build_device_factor(Factor& f) {
         group_of_root[k] = gmin;
       }
       const double maxb = 8.0 * *std::max_element(load.begin(), load.end());
-      return maxb / 25e9 + 20e-6 * (double)(f.nlevels - fz);
+      // + ~8 us per fused level: each is a block-barrier-separated pass with
+      // its own dependent latency (cfg2: picks 6 levels, 167 us for both
+      // sweeps, against 190 us at 7 without this term; cfg3 keeps 6)
+      return maxb / 25e9 + 20e-6 * (double)(f.nlevels - fz) + 8e-6 * (double)fz;
     };
     int best = 0;
     double best_t = 20e-6 * (double)f.nlevels;
