@@ -3,7 +3,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-fi
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo launches=$?
 ncu --set full --clock-control none --import-source on -k regex:k_cholesky_tiles -s 3 -c 1 -o gpurun_out/full_k_cholesky_tiles \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_chol.log 2>&1; echo chol=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_pcg$" -c 1 -o gpurun_out/full_k_pcg \
-    python tools/ncu_targets.py pcg > gpurun_out/ncu_pcg.log 2>&1; echo pcg=$?
-ncu --set full --clock-control none --import-source on -k regex:k_fw_level -s 20 -c 1 -o gpurun_out/full_k_fw_level \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_fw.log 2>&1; echo fw=$?
+ncu --set full --clock-control none --import-source on -k regex:k_dense_backward -s 3 -c 1 -o gpurun_out/full_k_dense_backward \
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bw.log 2>&1; echo bw=$?
