@@ -32,7 +32,22 @@
 
 #include "spb_internal.h"
 
+#include <chrono>
+#include <cstdio>
+
 namespace spb {
+// SPB_PRECOMPUTE_TIMING=1: per-phase wall times of Factor::build on stderr
+struct PhaseTimer {
+  bool on = getenv("SPB_PRECOMPUTE_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[precompute] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 
 // ----------------------------------------------------------------- host BLAS
 typedef void (*dgemm_t)(const char*, const char*, const int*, const int*, const int*, const double*,
@@ -251,6 +266,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
     for (int64_t p = Ap[j]; p < Ap[j + 1]; ++p)
       if (Ai[p] < 0 || Ai[p] > j) { set_error("input must be the upper triangle in CSC"); return SPB_ERR_ARG; }
 
+  PhaseTimer ptimer;
   // ---- 1. fill ordering of x1 (fperm: new -> old within x1)
   std::vector<int64_t> gp, gi;
   x1_graph(n1, Ap, Ai, gp, gi);
@@ -309,6 +325,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
   std::vector<int64_t> parent;
   etree_from_lower(n, rp, ri, parent);
 
+  ptimer.mark("ordering");
   // ---- 2. postorder of the x1 forest (parents >= n1 are virtual roots)
   if (ordering == 1 && n1 > 1) {
     std::vector<int64_t> head(n1, -1), next(n1, -1), stack, post;
@@ -362,6 +379,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
       }
   }
 
+  ptimer.mark("postorder");
   // ---- 3. column counts of L (columns < n1, all rows) via row subtrees
   std::vector<int64_t> colcount(n1, 1);
   {
@@ -385,6 +403,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
     for (int64_t p = cp[j]; p < cp[j + 1]; ++p)
       if (ci[p] == j) maxdiag = std::max(maxdiag, cx[p]);
 
+  ptimer.mark("column counts");
   // ---- 4. fundamental supernodes (+ relaxed amalgamation)
   std::vector<int64_t> nchild(n1, 0);
   for (int64_t j = 0; j < n1; ++j)
@@ -454,6 +473,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
     sn_parent[s] = (p >= 0 && p < n1) ? col2sn[p] : -1;
   }
 
+  ptimer.mark("supernodes");
   // ---- 5. supernodal row structures (children before parents: s ascending)
   std::vector<std::vector<int64_t>> children(nsuper);
   for (int64_t s = 0; s < nsuper; ++s)
@@ -496,6 +516,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
   Lval.assign(sn_valptr[nsuper], 0.0);
   Mval.assign(sn_valptr[nsuper], 0.0);
 
+  ptimer.mark("row structures");
   // ---- 6. numeric multifrontal factorization
   sigma0.assign((size_t)n2 * n2, 0.0);
   for (int64_t j = n1; j < n; ++j)  // A22 (lower)
@@ -505,6 +526,13 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
     }
   std::vector<std::vector<double>> upd(nsuper);
   std::vector<int64_t> pos(n, -1);
+  double blas_ms = 0.0;
+  auto timed = [&](auto&& fn) {
+    if (!ptimer.on) return fn();
+    auto t0 = std::chrono::steady_clock::now();
+    fn();
+    blas_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
   const double one = 1.0, mone = -1.0;
   bad_column = -1;
   for (int64_t s = 0; s < nsuper; ++s) {
@@ -531,7 +559,7 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
     }
     // partial factorization of the front
     int inc = as_int(nc), inr = as_int(nr), info = 0;
-    g_dpotrf("L", &inc, F.data(), &inr, &info);
+    timed([&] { g_dpotrf("L", &inc, F.data(), &inr, &info); });
     if (info > 0) { bad_column = f + info - 1; break; }
     for (int64_t k = 0; k < nc; ++k) {
       double d = F[(size_t)k * nr + k];
@@ -540,12 +568,12 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
     if (bad_column >= 0) break;
     if (nb > 0) {
       int inb = as_int(nb);
-      g_dtrsm("R", "L", "T", "N", &inb, &inc, &one, F.data(), &inr, F.data() + nc, &inr);
+      timed([&] { g_dtrsm("R", "L", "T", "N", &inb, &inc, &one, F.data(), &inr, F.data() + nc, &inr); });
       std::vector<double>& U = upd[s];
       U.assign((size_t)nb * nb, 0.0);
       for (int64_t b = 0; b < nb; ++b)
         for (int64_t a = b; a < nb; ++a) U[(size_t)b * nb + a] = F[(size_t)(nc + b) * nr + nc + a];
-      g_dsyrk("L", "N", &inb, &inc, &mone, F.data() + nc, &inr, &one, U.data(), &inb);
+      timed([&] { g_dsyrk("L", "N", &inb, &inc, &mone, F.data() + nc, &inr, &one, U.data(), &inb); });
       if (sn_parent[s] < 0) {
         // root of the x1 forest: all below rows are x2 -> extend-add into sigma0
         for (int64_t b = 0; b < nb; ++b) {
@@ -565,11 +593,11 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
       for (int64_t r = 0; r < nr; ++r) Ls[(size_t)c * nr + r] = (r < c) ? 0.0 : F[(size_t)c * nr + r];
     // partitioned inverse: Minv = inv(L_ss), W = L_below Minv
     std::memcpy(Ms, Ls, sizeof(double) * (size_t)nr * nc);
-    g_dtrtri("L", "N", &inc, Ms, &inr, &info);
+    timed([&] { g_dtrtri("L", "N", &inc, Ms, &inr, &info); });
     if (nb > 0) {
       // W = L_below * Minv  ==  solve W * L_ss = L_below
       int inb = as_int(nb);
-      g_dtrsm("R", "L", "N", "N", &inb, &inc, &one, Ls, &inr, Ms + nc, &inr);
+      timed([&] { g_dtrsm("R", "L", "N", "N", &inb, &inc, &one, Ls, &inr, Ms + nc, &inr); });
     }
     for (int64_t k = 0; k < nr; ++k) pos[rows[k]] = -1;
   }
@@ -581,6 +609,8 @@ int Factor::build(int64_t n_, int64_t n1_, const int64_t* Ap, const int64_t* Ai,
   for (int64_t i = 0; i < n2; ++i)
     for (int64_t j = 0; j < i; ++j) sigma0[(size_t)j * n2 + i] = sigma0[(size_t)i * n2 + j];
 
+  ptimer.mark("numeric factorization");
+  if (ptimer.on) fprintf(stderr, "[precompute]   of which host BLAS/LAPACK   %8.1f ms\n", blas_ms);
   // ---- 7. schedule metadata for the device solves
   sn_level.assign(nsuper, 0);
   nlevels = 0;
