@@ -40,6 +40,10 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 
+# BASELINE.json's metric, verbatim (both arms print it)
+METRIC = "PD frames/sec w/ collisions at 600K tets, 5% collision DOFs; Cholesky FP64 TFLOPS"
+
+
 def _env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
         os.environ.get("LOCAL_RANK", "0"))
@@ -207,7 +211,7 @@ def run_reference(args):
     sec, times = cpu_oracle_frames(sim, nf, threads)
     value = 1.0 / sec
     line = {
-        "impl": "reference", "metric": "PD frames/sec w/ collisions (600K tets, 5% collision DOFs)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sec, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
@@ -311,7 +315,7 @@ def run_b200(args):
     t_hbm = bytes_frame / (hbm_peak * 1e9) * 1e3
     achieved = chol_flops / (chol.value * 1e-3) / 1e12
     line = {
-        "metric": "PD frames/sec w/ collisions (600K tets, 5% collision DOFs); Cholesky FP64 TFLOPS",
+        "metric": METRIC,
         "value": replica_throughput(world, ms_frame), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_frame, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (lattice scene through the reference schema)",
