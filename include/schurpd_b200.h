@@ -289,6 +289,10 @@ int32_t spb_dense_get_matrix(spb_dense *d, double *h /* m x m row-major, symmetr
 int32_t spb_dense_get_factor(spb_dense *d, int32_t replica, double *chol /* m x m row-major, lower */);
 int32_t spb_dense_ipc_handle(spb_dense *d, uint8_t *out /* SPB_DENSE_IPC_BYTES */);
 int32_t spb_dense_open_peers(spb_dense *d, const uint8_t *handles /* nranks * SPB_DENSE_IPC_BYTES, rank order */);
+/* diagnostics: peer < 0 fills the own replica's first L tile (and 16 flag
+ * words) with `value`; peer >= 0 reads the first L value and flag word of the
+ * peer's IPC-mapped replica (peer slots in rank order, own rank skipped) */
+int32_t spb_dense_debug_replica(spb_dense *d, int32_t peer, double value, double *out_value, int32_t *out_flag);
 int32_t spb_dense_reset(spb_dense *d);
 int32_t spb_dense_launch(spb_dense *d);
 int32_t spb_dense_finish(spb_dense *d, double *ms, int64_t *info);

@@ -121,6 +121,7 @@ _SIGS = {
     "spb_dense_get_factor": ([P, I32, P], I32),
     "spb_dense_ipc_handle": ([P, P], I32),
     "spb_dense_open_peers": ([P, P], I32),
+    "spb_dense_debug_replica": ([P, I32, F64, P, P], I32),
     "spb_dense_reset": ([P], I32),
     "spb_dense_launch": ([P], I32),
     "spb_dense_finish": ([P, P, P], I32),

@@ -447,6 +447,30 @@ int32_t spb_dense_open_peers(spb_dense* d, const uint8_t* handles) {
   SPB_GUARD_END
 }
 
+// Diagnostics of the IPC plumbing without any kernel that waits on a peer:
+// write `value` into the own replica's first L tile and its flag words, or
+// read the first L value and flag word of peer slot `peer` (rank order,
+// own rank skipped) through the mapped allocation.
+int32_t spb_dense_debug_replica(spb_dense* d, int32_t peer, double value, double* out_value, int32_t* out_flag) {
+  SPB_GUARD_BEGIN
+  DCHECK(d);
+  if (peer < 0) {
+    std::vector<double> t(spb::TILE, value);
+    SPB_CUDA(cudaMemcpy(d->reps[0].L(d->lo), t.data(), sizeof(double) * spb::TILE, cudaMemcpyHostToDevice));
+    std::vector<int> f(16, (int)value);
+    SPB_CUDA(cudaMemcpy(d->reps[0].flags(d->lo), f.data(), sizeof(int) * 16, cudaMemcpyHostToDevice));
+    return SPB_OK;
+  }
+  if (peer >= (int)d->peers.size() || !out_value || !out_flag) {
+    spb::set_error("spb_dense_debug_replica: no such peer");
+    return SPB_ERR_ARG;
+  }
+  SPB_CUDA(cudaMemcpy(out_value, d->peers[peer].L(d->lo), sizeof(double), cudaMemcpyDeviceToHost));
+  SPB_CUDA(cudaMemcpy(out_flag, d->peers[peer].flags(d->lo), sizeof(int), cudaMemcpyDeviceToHost));
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
 int32_t spb_dense_reset(spb_dense* d) {
   SPB_GUARD_BEGIN
   DCHECK(d);
