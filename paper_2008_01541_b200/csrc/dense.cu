@@ -411,9 +411,11 @@ template <bool MULTI>
 // upd (optional): a swizzled tile U whose rank-64 update A -= U U^T is still
 // due (the diagonal task's sub-diagonal tile): warp 0 applies it to the first
 // 16x16 block and starts factoring while warps 1-7 apply the rest.
+// rel_flag (optional): the flag of that tile, released (value 2, and in the
+// peers' replicas at rel_idx) by warp 7 while warp 0 factors the first block.
 __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
                                    int* info, int* flag, int wr, int wc, int lane, const DensePeers& pr,
-                                   const double* upd) {
+                                   const double* upd, int* rel_flag = nullptr, int rel_idx = 0) {
   const int tid = threadIdx.x, warp = tid >> 5;
   POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
@@ -503,6 +505,12 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
       }
       potrf_diag16(S, DT, o, j, info, lane);
     } else {
+      if (kb == 0 && rel_flag && warp == NCONS / 32 - 1 && lane == 0) {
+        // every thread's stores of the tile precede the barriers above
+        fence_tile_stores<MULTI>();
+        st_release(rel_flag, 2);
+        if (MULTI) release_peers(pr, rel_idx, 2);
+      }
       if (kb == 0 && upd) {
         // the rest of A -= U U^T: lower 8x8 blocks of rows 16..63 (33 blocks)
         constexpr int NB = 33;
@@ -761,14 +769,11 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
         for (int p = 0; p < d.peers.n; ++p)
           acc_to_swz(out, d.peers.L[p] + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
       // its rank-64 update A -= L(j, j-1) L(j, j-1)^T is applied inside the
-      // factorization (from the scratch copy), off the chain but its first block
+      // factorization (from the scratch copy), off the chain but its first
+      // block; the tile's release (flag 2) is issued inside the factorization
+      // too, by a warp off the pivot chain, after the factorization's first
+      // CTA barrier has ordered every thread's stores before it
       fence_proxy_async_global();
-      fence_tile_stores<MULTI>();
-      cons_sync();
-      if (tid == 0) {
-        st_release(d.flags + tidx(j, j - 1), 2);
-        if (MULTI) release_peers(d.peers, tidx(j, j - 1), 2);
-      }
       if (lane == 0) {
         mbar_arrive(&sm.empty[sa]);
         mbar_arrive(&sm.empty[sb]);
@@ -780,7 +785,8 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       // the producer is parked: the whole stage area holds the augmented panel + D^-T
       potrf_blocked_tile<MULTI>(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
                                 d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane, d.peers,
-                                j > 0 ? sm.scratch : nullptr);
+                                j > 0 ? sm.scratch : nullptr, j > 0 ? d.flags + tidx(j, j - 1) : nullptr,
+                                j > 0 ? tidx(j, j - 1) : 0);
     } else if (i == j + 1 && !rhs) {
       // sub-diagonal tile: publish the partial sum; diagonal task j+1 finalizes it
       acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
