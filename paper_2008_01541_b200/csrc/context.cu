@@ -1208,9 +1208,7 @@ int32_t spb_ctx_trace_cholesky(spb_ctx* cp, uint64_t* out, int32_t* tasks_out, i
   SPB_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * 4 * c->ntasks));
   spb::DenseDev dd = c->dd;
   dd.trace = tr;
-  const char* nd = getenv("SPB_CHOL_NODEPS");  // diagnostics: no dependency waits
-  SPB_CUDA(cudaMemsetAsync(c->flags.p, (nd && nd[0] == '1') ? 2 : 0,
-                           sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
+  SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
   SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
   spb::launch_cholesky_tiles(c->st, dd, c->tasks.p, c->ntasks, c->chol_grid);
   SPB_CUDA(cudaStreamSynchronize(c->st));
@@ -1376,12 +1374,11 @@ int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
   SPB_CUDA(cudaEventCreate(&e0));
   SPB_CUDA(cudaEventCreate(&e1));
   float tot = 0;
-  // SPB_CHOL_NODEPS=1 (diagnostics only): every readiness flag preset, so the
-  // launch measures raw task throughput without dependency waits (result invalid).
-  const char* nd = getenv("SPB_CHOL_NODEPS");
-  const int preset = (nd && nd[0] == '1') ? 2 : 0;  // bytes of 2: every flag >= 2
+  // (a former diagnostic preset every flag to time the task list without
+  // dependencies; it can deadlock once a late partial overwrites its
+  // finalized flag, so it is gone)
   for (int r = 0; r < reps; ++r) {
-    SPB_CUDA(cudaMemsetAsync(c->flags.p, preset, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
+    SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
     SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
     SPB_CUDA(cudaEventRecord(e0, c->st));
     spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid);

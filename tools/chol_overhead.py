@@ -1,6 +1,5 @@
 """Per-task cost model of the tile Cholesky from a traced launch (diagnostics):
-duration = a + b * k_steps, fitted per task kind; run with SPB_CHOL_NODEPS=1
-for the dependency-free throughput picture."""
+duration = a + b * k_steps, fitted per task kind."""
 import ctypes, sys
 from pathlib import Path
 import numpy as np
