@@ -12,8 +12,6 @@ sim = P.Simulation(P.parse_scenario(config_yaml(cfgname)), diagnostics=False)
 for _ in range(3): sim.step()
 ds = device_scene(sim.model, sim.system)
 m = sim.partition.n2
-for mode in (os.environ.get("SPB_PROBE_MODES", "0,1").split(",")):
-    os.environ["SPB_CHOL_NODEPS"] = mode
-    ms = ctypes.c_double()
-    _native.check(_native.lib().spb_ctx_bench_cholesky(ds.handle, 5, ctypes.byref(ms)))
-    print(f"nodeps={mode}: {ms.value:.3f} ms  {m**3/3/ms.value/1e9:.2f} TF")
+ms = ctypes.c_double()
+_native.check(_native.lib().spb_ctx_bench_cholesky(ds.handle, 5, ctypes.byref(ms)))
+print(f"{cfgname}: {ms.value:.3f} ms  {m**3/3/ms.value/1e9:.2f} TF")
