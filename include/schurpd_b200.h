@@ -214,6 +214,21 @@ int32_t spb_ctx_frame_pcg(spb_ctx *ctx, const double *att_targets, int32_t num_c
                           const spb_posed_collider *colliders, double *x, uint8_t *active, double *target,
                           const spb_step_config *cfg, double tol, int64_t max_iters, spb_frame_metrics *metrics,
                           int64_t *pcg_iterations);
+/* A batch of frames (BASELINE config 5 through the public API): the
+ * arguments of spb_ctx_frame per context; every frame is in flight before
+ * the host waits on any. metrics: n entries. Returns the first error. */
+typedef struct {
+  const double *att_targets;
+  int32_t num_colliders;
+  const spb_posed_collider *colliders;
+  double *x;
+  uint8_t *active;
+  double *target;
+  double *f_tilde2;
+  double *u2_accum;
+} spb_frame_io;
+int32_t spb_frame_batch(spb_ctx **ctxs, int32_t n, const spb_frame_io *io, const spb_step_config *cfg,
+                        spb_frame_metrics *metrics);
 /* Download state; any pointer may be NULL to skip that field. */
 int32_t spb_ctx_get_state(spb_ctx *ctx, double *x, double *R, double *Q, uint8_t *active, double *target,
                           double *f_tilde2, double *u2_accum);

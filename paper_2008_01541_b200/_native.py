@@ -65,6 +65,11 @@ class StepConfig(ctypes.Structure):
                 ("unused", I32), ("early_exit_residual", F64)]
 
 
+class FrameIO(ctypes.Structure):
+    _fields_ = [("att_targets", P), ("num_colliders", I32), ("colliders", P), ("x", P), ("active", P),
+                ("target", P), ("f_tilde2", P), ("u2_accum", P)]
+
+
 class FrameMetricsC(ctypes.Structure):
     _fields_ = [("t_local_ms", F64), ("t_forward_ms", F64), ("t_detect_ms", F64), ("t_dense_ms", F64),
                 ("t_backward_ms", F64), ("t_total_ms", F64), ("energy", F64), ("active_proxies", I64),
@@ -102,6 +107,7 @@ _SIGS = {
     "spb_ctx_trace_dense_backward": ([P, P, P], I32),
     "spb_bench_batch": ([P, I32, P, I32, P], I32),
     "spb_ctx_set_concurrency": ([P, I32], I32),
+    "spb_frame_batch": ([P, I32, P, P, P], I32),
     "spb_ctx_trace_cholesky": ([P, P, P, P], I32),
     "spb_op_deformation_gradients": ([I64, P, P, I64, P, I64, P, P], I32),
     "spb_op_svd": ([I64, P, P, P, P, P, P, F64, F64], I32),

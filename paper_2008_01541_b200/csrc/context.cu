@@ -256,30 +256,43 @@ static int io_upload(Ctx* c, const IoList& l, bool sync = true) {
   return SPB_OK;
 }
 
-static int io_download(Ctx* c, const IoList& l, cudaStream_t st = nullptr, bool wait_state = false) {
-  if (!st) st = c->st;
+// The download in two halves (enqueue; then wait and unstage), so a batch of
+// contexts can have every frame in flight before the host waits on any.
+struct IoPending {
+  bool staged[8] = {};
+};
+static int io_download_enqueue(Ctx* c, const IoList& l, cudaStream_t st, bool wait_state, IoPending& pend) {
   TRY(c->io_reserve(l.total));
   if (wait_state) SPB_CUDA(cudaStreamWaitEvent(st, c->ev_state, 0));
   size_t off = 0;
-  bool staged[8] = {};
   for (int i = 0; i < l.n; ++i) {
+    pend.staged[i] = false;
     if (host_pinned(l.items[i].host)) {
       SPB_CUDA(cudaMemcpyAsync(l.items[i].host, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, st));
       continue;
     }
-    staged[i] = true;
+    pend.staged[i] = true;
     SPB_CUDA(cudaMemcpyAsync(c->io_host + off, l.items[i].dev, l.items[i].bytes, cudaMemcpyDeviceToHost, st));
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
+  return SPB_OK;
+}
+static int io_download_finish(Ctx* c, const IoList& l, cudaStream_t st, const IoPending& pend) {
   SPB_CUDA(cudaStreamSynchronize(st));
   if (st != c->st) SPB_CUDA(cudaStreamSynchronize(c->st));
-  off = 0;
+  size_t off = 0;
   for (int i = 0; i < l.n; ++i) {
-    if (!staged[i]) continue;
+    if (!pend.staged[i]) continue;
     memcpy(l.items[i].host, c->io_host + off, l.items[i].bytes);
     off += (l.items[i].bytes + 255) & ~size_t(255);
   }
   return SPB_OK;
+}
+static int io_download(Ctx* c, const IoList& l, cudaStream_t st = nullptr, bool wait_state = false) {
+  if (!st) st = c->st;
+  IoPending pend;
+  TRY(io_download_enqueue(c, l, st, wait_state, pend));
+  return io_download_finish(c, l, st, pend);
 }
 
 int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
@@ -803,8 +816,11 @@ int Ctx::enqueue_metrics(cudaEvent_t* ev) {
 using spb::Ctx;
 using spb::Factor;
 using spb::IoList;
+using spb::IoPending;
 using spb::io_upload;
 using spb::io_download;
+using spb::io_download_enqueue;
+using spb::io_download_finish;
 
 // ================================================================== C ABI
 extern "C" {
@@ -1099,6 +1115,51 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
   TRY(io_download(c, down, c->st_io, true));
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return frame_finish(c, m);
+  SPB_GUARD_END
+}
+
+// A batch of frames (BASELINE config 5 through the public API): every
+// context's pose and state go up and its frame graph is launched before the
+// host waits on any, so the scenes' frames and transfers overlap; then each
+// context's state comes back as in spb_ctx_frame.
+int32_t spb_frame_batch(spb_ctx** ctxs, int32_t n, const spb_frame_io* io, const spb_step_config* cfg,
+                        spb_frame_metrics* metrics) {
+  SPB_GUARD_BEGIN
+  if (n <= 0 || !ctxs || !io || !cfg || !metrics) { spb::set_error("spb_frame_batch: bad arguments"); return SPB_ERR_ARG; }
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<IoList> downs(n);
+  std::vector<IoPending> pend(n);
+  for (int k = 0; k < n; ++k) {
+    Ctx* c = reinterpret_cast<Ctx*>(ctxs[k]);
+    const spb_frame_io& f = io[k];
+    memset(&metrics[k], 0, sizeof(spb_frame_metrics));
+    SPB_CUDA(cudaSetDevice(c->device));
+    SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
+    TRY(pose_upload(c, f.att_targets, f.num_colliders, f.colliders));
+    IoList up;
+    up.add(c->x.p, f.x, sizeof(double) * 3 * c->n);
+    if (c->P) up.add(c->active.p, f.active, c->P);
+    if (c->P) up.add(c->target.p, f.target, sizeof(double) * 3 * c->P);
+    TRY(io_upload(c, up, false));
+    TRY(frame_enqueue(c, cfg, nullptr));
+    IoList& down = downs[k];
+    down.add(c->x.p, f.x, sizeof(double) * 3 * c->n);
+    if (c->P) down.add(c->active.p, f.active, c->P);
+    if (c->P) down.add(c->target.p, f.target, sizeof(double) * 3 * c->P);
+    if (c->n2) down.add(c->f_tilde2.p, f.f_tilde2, sizeof(double) * 3 * c->n2);
+    if (c->n2) down.add(c->u2acc.p, f.u2_accum, sizeof(double) * 3 * c->n2);
+    TRY(io_download_enqueue(c, down, c->st_io, true, pend[k]));
+  }
+  int rc = SPB_OK;
+  for (int k = 0; k < n; ++k) {
+    Ctx* c = reinterpret_cast<Ctx*>(ctxs[k]);
+    SPB_CUDA(cudaSetDevice(c->device));
+    TRY(io_download_finish(c, downs[k], c->st_io, pend[k]));
+    metrics[k].t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const int r = frame_finish(c, &metrics[k]);
+    if (r != SPB_OK && rc == SPB_OK) rc = r;
+  }
+  return rc;
   SPB_GUARD_END
 }
 

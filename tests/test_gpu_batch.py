@@ -74,3 +74,29 @@ def test_concurrency_hint_is_bitwise_neutral():
     a.step()
     b.step()
     assert np.array_equal(a.state.x, b.state.x)
+
+
+def test_step_batch_matches_sequential_steps():
+    """harness.step_batch (one spb_frame_batch call: every scene's frame in
+    flight before the host waits) leaves each scene exactly where step() would."""
+    def sims():
+        out = []
+        for i in range(3):
+            s = P.Simulation(P.parse_scenario(block_yaml(16, 10, 8, 0.75, vel=-0.004 * (1 + i / 64.0) * 4)),
+                             diagnostics=False)
+            if out:
+                s.system = out[0].system
+            out.append(s)
+        return out
+
+    a, b = sims(), sims()
+    for _ in range(4):
+        ma = P.step_batch(a)
+        mb = [s.step() for s in b]
+    for sa, sb, x, y in zip(a, b, ma, mb):
+        assert np.array_equal(sa.state.x, sb.state.x)
+        assert np.array_equal(sa.state.active.active, sb.state.active.active)
+        assert np.array_equal(sa.state.f_tilde2, sb.state.f_tilde2)
+        assert x.active_proxies == y.active_proxies and x.energy == y.energy
+    assert a[0].state.active.count > 0
+    assert not np.array_equal(a[0].state.x, a[2].state.x)
