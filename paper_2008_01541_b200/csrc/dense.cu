@@ -197,6 +197,69 @@ __device__ __forceinline__ void mma_ab(Acc& acc, const double* sA, const double*
   }
 }
 
+// out = A * U with U = inv(L_jj)^T upper triangular (U[k][n] = 0 for k > n,
+// stored as exact zeros). Column block cb (16 columns) needs only k < 16(cb+1),
+// so the warp tiling pairs blocks {0,3} and {1,2}: warp w takes rows
+// 16(w >> 1) .. +15 of both blocks of its pair and issues 80 DMMAs where the
+// dense 32 x 16 tiling issues 128. The skipped products are zero and come last
+// in k order, so the sums are those of the dense product.
+struct TriAcc {
+  double c[2][2][2][2];  // [pair block][mb][nb][2]
+};
+__device__ __forceinline__ int tri_block(int warp, int blk) { return (warp & 1) ? 1 + blk : 3 * blk; }
+__device__ __forceinline__ void mma_ab_upper(TriAcc& acc, const double* sA, const double* sU, int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3, gq = g & 3;
+  const int cb0 = tri_block(warp, 0), cb1 = tri_block(warp, 1);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) acc.c[q][mb][nb][0] = acc.c[q][mb][nb][1] = 0.0;
+  const double* pa = sA + ((warp >> 1) * 16 + g) * TS + t;
+  int ob[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) ob[b] = 4 * (b ^ gq);
+  const double* pb[2][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) pb[q][nb] = sU + t * TS + (((q ? cb1 : cb0) * 16 + nb * 8 + g) ^ (t << 2));
+#pragma unroll
+  for (int kb = 0; kb < 4; ++kb) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int k0 = kb * 16 + 4 * b;
+      double av[2];
+#pragma unroll
+      for (int mb = 0; mb < 2; ++mb) av[mb] = pa[ob[b] + mb * 8 * TS + kb * 16];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (kb > (q ? cb1 : cb0)) continue;  // warp-uniform
+        double bv[2];
+#pragma unroll
+        for (int nb = 0; nb < 2; ++nb) bv[nb] = pb[q][nb][k0 * TS];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < 2; ++nb) dmma(acc.c[q][mb][nb][0], acc.c[q][mb][nb][1], av[mb], bv[nb]);
+      }
+    }
+  }
+}
+__device__ __forceinline__ void tri_to_swz(const TriAcc& acc, double* s, int warp, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int r = (warp >> 1) * 16 + mb * 8 + g, c = tri_block(warp, q) * 16 + nb * 8 + 2 * t;
+        *reinterpret_cast<double2*>(s + swz(r, c)) = make_double2(acc.c[q][mb][nb][0], acc.c[q][mb][nb][1]);
+      }
+}
+
 // fragment (row r0+g, cols c0+2t, c0+2t+1) <-> swizzled tiles (smem or global)
 template <typename F>
 __device__ __forceinline__ void acc_foreach(int wr, int wc, int lane, F f) {
@@ -758,16 +821,14 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       const int sb = it % NSTAGE;  // slot 1: inv(L_{j-1,j-1})^T
       mbar_wait(&sm.full[sb], (it / NSTAGE) & 1);
       ++it;
-      Acc out;
-      acc_zero(out);
-      mma_ab(out, sm.slot(sa, 0), sm.slot(sb, 1), wr, wc, lane);
+      TriAcc out;
+      mma_ab_upper(out, sm.slot(sa, 0), sm.slot(sb, 1), warp, lane);
       cons_sync();  // every warp has finished reading both stages
       double* scratch = sm.scratch;
-      acc_to_swz(out, scratch, wr, wc, lane);
-      acc_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+      tri_to_swz(out, scratch, warp, lane);
+      tri_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, warp, lane);
       if (MULTI)
-        for (int p = 0; p < d.peers.n; ++p)
-          acc_to_swz(out, d.peers.L[p] + (size_t)tidx(j, j - 1) * TILE, wr, wc, lane);
+        for (int p = 0; p < d.peers.n; ++p) tri_to_swz(out, d.peers.L[p] + (size_t)tidx(j, j - 1) * TILE, warp, lane);
       // its rank-64 update A -= L(j, j-1) L(j, j-1)^T is applied inside the
       // factorization (from the scratch copy), off the chain but its first
       // block; the tile's release (flag 2) is issued inside the factorization
@@ -797,16 +858,15 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       cons_sync();
       s = it % NSTAGE;
       mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-      Acc out;
-      acc_zero(out);
-      mma_ab(out, sm.scratch, sm.slot(s, 1), wr, wc, lane);  // acc * inv(L_jj)^T = acc * LinvT
+      TriAcc out;
+      mma_ab_upper(out, sm.scratch, sm.slot(s, 1), warp, lane);  // acc * inv(L_jj)^T = acc * LinvT
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       ++it;
       double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
-      acc_to_swz(out, dst, wr, wc, lane);
+      tri_to_swz(out, dst, warp, lane);
       if (MULTI)  // tile-cyclic: no RHS row
-        for (int p = 0; p < d.peers.n; ++p) acc_to_swz(out, d.peers.L[p] + (size_t)tidx(i, j) * TILE, wr, wc, lane);
+        for (int p = 0; p < d.peers.n; ++p) tri_to_swz(out, d.peers.L[p] + (size_t)tidx(i, j) * TILE, warp, lane);
     }
     if (d.trace && tid == 0) t_fin = globaltimer();
     fence_proxy_async_smem();    // generic smem writes before later bulk copies into the stages
