@@ -33,7 +33,11 @@ constexpr int PTILE = TILE;              // doubles per smem stage tile (swizzle
 constexpr int NSTAGE = 3;
 constexpr int NCONS = 256;               // consumer threads (8 warps)
 constexpr int NTHREADS = NCONS + 32;     // + 1 producer warp
-constexpr int LDP = 66;                  // plain row stride of the potrf scratch
+constexpr int LDP = 66;
+// RHS row tiles move only their first 8 rows (g^T in rows 0..2, zeros in 3..7;
+// swz keeps every row inside its own 64 doubles). Rows 8..63 of a Y tile are
+// scratch that no reader uses (each output row depends on its own input row).
+constexpr int RHS_BYTES = 8 * TS * 8;                  // plain row stride of the potrf scratch
 
 __host__ __device__ __forceinline__ int tidx(int i, int j) { return i * (i + 1) / 2 + j; }
 int dense_tile_count(int N) { return N * (N + 1) / 2; }
@@ -165,6 +169,33 @@ __device__ __forceinline__ void mma_abt(Acc& acc, const double* sA, const double
       for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb) dmma(acc.c[mb][nb][0], acc.c[mb][nb][1], av[mb], bv[nb]);
+    }
+  }
+}
+
+// The RHS row's k-step: only rows 0..7 of A (g^T packed in rows 0..2, rows
+// 3..7 zero) carry data, so only the warps of rows 0..31 (wr = 0) work, on
+// their first m8 block: 1/8 of the DMMAs of a full tile, with the same
+// fragment order as mma_abt for those rows (bit-identical results).
+template <bool NEG>
+__device__ __forceinline__ void mma_abt_m8(Acc& acc, const double* sA, const double* sB, int wc, int lane) {
+  const int g = lane >> 2, t = lane & 3, gq = g & 3;
+  const double* pa = sA + g * TS + t;
+  const double* pb = sB + (wc * 16 + g) * TS + t;
+  int ob[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) ob[b] = 4 * (b ^ gq);
+#pragma unroll
+  for (int a16 = 0; a16 < TS; a16 += 16) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const double v = pa[ob[b] + a16];
+      const double av = NEG ? -v : v;
+      double bv[2];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) bv[nb] = pb[ob[b] + nb * 8 * TS + a16];
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) dmma(acc.c[0][nb][0], acc.c[0][nb][1], av, bv[nb]);
     }
   }
 }
@@ -707,12 +738,12 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
   __syncthreads();
   int it = 0;  // stage-use counter, advanced identically by producer and consumers
   if (producer) {
-    auto fill = [&](const double* a, const double* b, int slot_a) {
+    auto fill = [&](const double* a, const double* b, int slot_a, int abytes = TILE_BYTES) {
       const int s = it % NSTAGE;
       if (lane == 0) {
         mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
-        mbar_expect_tx(&sm.full[s], (b ? 2 : 1) * TILE_BYTES);
-        bulk_g2s(sm.slot(s, slot_a), a, TILE_BYTES, &sm.full[s]);
+        mbar_expect_tx(&sm.full[s], abytes + (b ? TILE_BYTES : 0));
+        bulk_g2s(sm.slot(s, slot_a), a, abytes, &sm.full[s]);
         if (b) bulk_g2s(sm.slot(s, 1), b, TILE_BYTES, &sm.full[s]);
       }
       __syncwarp();
@@ -740,7 +771,7 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       const int i = ij.x, j = ij.y;
       const bool rhs = (i == N);
       const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
-      fill(src, nullptr, 0);
+      fill(src, nullptr, 0, rhs ? RHS_BYTES : TILE_BYTES);
       if (i == j) {
         // diagonal task: A = B = L_jk (one copy), then the partial sum of the
         // sub-diagonal tile (j, j-1) with inv(L_{j-1,j-1})^T for its finalize
@@ -763,7 +794,8 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
           if (rhs) wait_ready(d.flags + ntiles + k, 1);
           else tile_ready(i, k);
           tile_ready(j, k);
-          fill(rhs ? d.Y + (size_t)k * TILE : d.L + (size_t)tidx(i, k) * TILE, d.L + (size_t)tidx(j, k) * TILE, 0);
+          if (rhs) fill(d.Y + (size_t)k * TILE, d.L + (size_t)tidx(j, k) * TILE, 0, RHS_BYTES);
+          else fill(d.L + (size_t)tidx(i, k) * TILE, d.L + (size_t)tidx(j, k) * TILE, 0);
         }
         if (i != j + 1 || rhs) {
           wait_ready(d.flags + tidx(j, j), 1);
@@ -806,7 +838,8 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       // ---- left-looking accumulation
       s = it % NSTAGE;
       mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
-      mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, i == j ? 0 : 1), wr, wc, lane);
+      if (!rhs) mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, i == j ? 0 : 1), wr, wc, lane);
+      else if (wr == 0) mma_abt_m8<true>(acc, sm.slot(s, 0), sm.slot(s, 1), wc, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.empty[s]);
       ++it;
