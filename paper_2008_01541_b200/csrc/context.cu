@@ -565,6 +565,12 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
         launches++;
       }
       launch_local_forces(st_aux, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
+      // the first pass's factorization flags, task counter and backward-chain
+      // rows are reset here, off the path from g to the factorization
+      SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st_aux));
+      SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st_aux));
+      dense_backward_preset(st_aux, dd, xrows.p);
+      SPB_CUDA(cudaMemsetAsync(u2acc.p, 0, sizeof(double) * 3 * n2, st_aux));
       SPB_CUDA(cudaEventRecord(ev_pre, st_aux));
     }
     // (1) local step on E_alpha fused with (2) the alpha element forces
@@ -579,7 +585,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
     } else if (n2 > 0) {
       SPB_CUDA(cudaMemcpyAsync(f_tilde2.p, b.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice, st));
     }
-    if (n2 > 0) SPB_CUDA(cudaMemsetAsync(u2acc.p, 0, sizeof(double) * 3 * n2, st));
+    if (n2 > 0 && !pre) SPB_CUDA(cudaMemsetAsync(u2acc.p, 0, sizeof(double) * 3 * n2, st));
     if (ev && o == outer - 1) SPB_CUDA(mark_phase(ev, 2, st));
     for (int it = 0; it < inner; ++it) {
       bool fresh = cadence == SPB_CADENCE_INNER || (cadence == SPB_CADENCE_FRAME && !first_detection_done);
@@ -600,10 +606,13 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       launch_build_g(st, n2, f_tilde2.p, gb_ptr.p, gb_src.p, Gb.p, nbeta, P_, tets.p, x.p, active.p, target.p,
                      gc_ptr.p, gc_src.p, g.p, Y.p);
       // (4.3)+(4.5) H = sigma0 + C22, LL^T = H, y = L^-1 g (one persistent launch), u2 = L^-T y
-      SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
-      SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
+      const bool preset = pre && it == 0;  // reset on the aux stream (joined through ev_pre)
+      if (!preset) {
+        SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
+        SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
+      }
       launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid);
-      launch_dense_backward(st, dd, xrows.p, u2.p);
+      launch_dense_backward(st, dd, xrows.p, u2.p, nullptr, preset);
       // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual.
       // In the last pass nothing downstream of the backward sweep needs f~2:
       // u2_accum is updated on the main stream (it feeds the sweep) and the

@@ -1265,15 +1265,19 @@ void launch_cholesky_ranks(cudaStream_t st, const DenseRankJob* jobs, int P, int
   k_cholesky_ranks<<<grid, NTHREADS, smem, st>>>(jobs, P);
 }
 
+void dense_backward_preset(cudaStream_t st, const DenseDev& d, double* xrows) {
+  cudaMemsetAsync(xrows, 0xff, sizeof(double) * 3 * TS * (size_t)d.N, st);  // BW_EMPTY everywhere
+}
+
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u,
-                           unsigned long long* trace) {
+                           unsigned long long* trace, bool preset) {
   static bool attr = false;
   const size_t smem = sizeof(double) * BW_SMEM_DOUBLES;
   if (!attr) {
     cudaFuncSetAttribute(k_dense_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  cudaMemsetAsync(xrows, 0xff, sizeof(double) * 3 * TS * (size_t)d.N, st);  // BW_EMPTY everywhere
+  if (!preset) dense_backward_preset(st, d, xrows);
   k_dense_backward<<<d.N, 256, smem, st>>>(d, xrows, u, d.m, trace);
 }
 

@@ -92,7 +92,8 @@ int dense_tile_owner(int i, int j, int nranks);
 std::vector<int2> cholesky_rank_tasks(int N, int rank, int nranks, int lead);
 constexpr int CHOL_LEAD = 2;
 void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, double* u,
-                           unsigned long long* trace = nullptr);
+                           unsigned long long* trace = nullptr, bool preset = false);
+void dense_backward_preset(cudaStream_t st, const DenseDev& d, double* xrows);  // xrows <- sentinel
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial);
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out);
 
