@@ -724,6 +724,9 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
   const int wr = warp >> 2, wc = warp & 3;
   const int N = d.N;
   const int ntiles = N * (N + 1) / 2;
+  // a PDL successor (the frame's dense backward) may be scheduled onto the
+  // SMs this grid frees in its tail; it waits on the tile flags itself
+  if (tid == 0) pdl_trigger();
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -1014,7 +1017,8 @@ __device__ __forceinline__ double bw_reduce(const double* part, int tid) {
 
 __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __restrict__ xrows /* N*3*64 */,
                                                         double* __restrict__ u, int m,
-                                                        unsigned long long* __restrict__ trace /* 5 per CTA or null */) {
+                                                        unsigned long long* __restrict__ trace /* 5 per CTA or null */,
+                                                        int await_flags) {
   unsigned long long tt[5] = {0, 0, 0, 0, 0};
   if (trace && threadIdx.x == 0) tt[0] = globaltimer();
   extern __shared__ double bw_sm[];
@@ -1032,6 +1036,24 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
   const int j = N - 1 - blockIdx.x;
   const int tid = threadIdx.x;
   const int c = tid & 63, grp = tid >> 6;  // 4 groups x 64 columns
+  if (await_flags) {
+    // launched programmatically behind the factorization: column j of L,
+    // inv(L_jj)^T and y_j are read only once their flags are released
+    if (tid < 32) {
+      const int ntiles = N * (N + 1) / 2;
+      for (int i = j + tid; i <= N; i += 32) {
+        const int* f = i == N ? d.flags + ntiles + j : d.flags + tidx(i, j);
+        const int v = (i == j + 1 && i < N) ? 2 : 1;  // the sub-diagonal tile is final at 2
+        // bounded: a flag that never comes traps instead of hanging the device
+        for (long long spin = 0; ld_relaxed(f) < v; ++spin) {
+          if (spin > (1ll << 24)) __trap();
+          __nanosleep(256);
+        }
+      }
+      fence_acq_rel_gpu();
+    }
+    __syncthreads();
+  }
   // ---- prologue (off the chain): W, L_{j+1,j}, L_{j+2,j} -> smem; M = L_{j+1,j} W
   for (int q = tid; q < TILE; q += 256) {
     const int k = q >> 6, cc = q & 63;
@@ -1277,8 +1299,14 @@ void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, do
     cudaFuncSetAttribute(k_dense_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  if (!preset) dense_backward_preset(st, d, xrows);
-  k_dense_backward<<<d.N, 256, smem, st>>>(d, xrows, u, d.m, trace);
+  if (!preset) {
+    dense_backward_preset(st, d, xrows);
+    k_dense_backward<<<d.N, 256, smem, st>>>(d, xrows, u, d.m, trace, 0);
+  } else {
+    // rows preset off the path: start behind the factorization (PDL) and
+    // wait on its tile flags, so the prologues run in its tail
+    launch_pdl(k_dense_backward, dim3(d.N), dim3(256), smem, st, d, xrows, u, d.m, trace, 1);
+  }
 }
 
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial) {
