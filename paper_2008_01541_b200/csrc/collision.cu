@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(256) k_build_g(int m, const double* __restrict
                                                  const double* __restrict__ target, const int* __restrict__ cptr,
                                                  const int* __restrict__ csrc, double* __restrict__ g,
                                                  double* __restrict__ ytile /* RHS tile row or null */) {
+  if (threadIdx.x == 0) pdl_trigger();  // the factorization behind may start; its RHS row waits for g
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m) return;
   double b0 = 0.0, b1 = 0.0, b2 = 0.0;

@@ -611,7 +611,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
         SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
         SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
       }
-      launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid);
+      launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid, preset);
       launch_dense_backward(st, dd, xrows.p, u2.p, nullptr, preset);
       // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual.
       // In the last pass nothing downstream of the backward sweep needs f~2:

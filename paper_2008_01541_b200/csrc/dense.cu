@@ -774,6 +774,12 @@ __device__ __forceinline__ void cholesky_body(const DenseDev& d, const int2* __r
       const int i = ij.x, j = ij.y;
       const bool rhs = (i == N);
       const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
+      if (rhs && lane == 0) {
+        // launched programmatically behind build_g: g is complete only after
+        // the predecessor grid (no-op in an ordinary launch)
+        pdl_wait();
+        fence_proxy_async_global();
+      }
       fill(src, nullptr, 0, rhs ? RHS_BYTES : TILE_BYTES);
       if (i == j) {
         // diagonal task: A = B = L_jk (one copy), then the partial sum of the
@@ -1267,12 +1273,16 @@ __global__ void k_sym_gemv_reduce(DenseDev d, const double* __restrict__ partial
 }
 
 // ------------------------------------------------------------- launchers
-void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid) {
+void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid, bool pdl) {
   static bool attr = false;
   size_t smem = cholesky_smem_bytes();
   if (!attr) {
     cudaFuncSetAttribute(k_cholesky_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
+  }
+  if (pdl) {
+    launch_pdl(k_cholesky_tiles, dim3(grid), dim3(NTHREADS), smem, st, d, tasks, ntasks);
+    return;
   }
   k_cholesky_tiles<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
 }

@@ -83,7 +83,8 @@ struct DenseRankJob {
 };
 int dense_tile_count(int N);
 size_t cholesky_smem_bytes();
-void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid);
+// pdl: launched programmatically behind build_g (only the RHS row waits for it)
+void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid, bool pdl = false);
 std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead);
 // P ranks (real: one job per process, P = 1 per launch; emulated: one launch
 // over all ranks' replicas, CTA b serving rank b % P)
