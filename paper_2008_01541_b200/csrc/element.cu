@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(128) k_local_forces(int nsub, const int* __res
                                                       const double* __restrict__ vol, int64_t ne,
                                                       double* __restrict__ R, double* __restrict__ Q,
                                                       ElemParams p, double* __restrict__ G, int project) {
+  if (threadIdx.x == 0) pdl_trigger();  // the node gather behind may launch (it waits for G)
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nsub) return;
   int64_t e = sub ? sub[i] : i;
@@ -283,6 +284,8 @@ __global__ void __launch_bounds__(256) k_gather_forces(int nout, const int* __re
                                                        const double* __restrict__ ak,
                                                        const double* __restrict__ atgt,
                                                        const double* __restrict__ x, double* __restrict__ out) {
+  if (threadIdx.x == 0) pdl_trigger();  // the forward sweep behind waits for b itself
+  pdl_wait();                           // G of the element kernel before
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= nout) return;
   double f0 = 0.0, f1 = 0.0, f2 = 0.0;
@@ -401,8 +404,8 @@ void launch_gather_forces(cudaStream_t st, int nout, const int* ptr, const int* 
                           const int* out_node, const int* aptr, const int* aidx, const double* ak,
                           const double* atgt, const double* x, double* out) {
   if (nout <= 0) return;
-  k_gather_forces<<<ceil_div(nout, 256), 256, 0, st>>>(nout, ptr, src, G, nsub, out_node, aptr, aidx, ak, atgt,
-                                                       x, out);
+  launch_pdl(k_gather_forces, dim3(ceil_div(nout, 256)), dim3(256), 0, st, nout, ptr, src, G, nsub, out_node, aptr,
+             aidx, ak, atgt, x, out);
 }
 
 int energy_blocks(int64_t ne) { return ceil_div(ne, 256); }
