@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(256) k_inner_update(int m, const double* __res
 // through fill_perm, solver.py:445).
 __global__ void k_scatter_add(int cnt, const int* __restrict__ node, const double* __restrict__ X,
                               double* __restrict__ x) {
+  pdl_wait();  // X of the backward sweep's last launch
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= 3 * cnt) return;
   int row = k / 3, q = k % 3;
@@ -206,7 +207,7 @@ void launch_u2acc_to_xf(cudaStream_t st, int m, const double* u2, double* u2acc,
 
 void launch_scatter_add(cudaStream_t st, int cnt, const int* node, const double* X, double* x) {
   if (cnt <= 0) return;
-  k_scatter_add<<<ceil_div(3 * (int64_t)cnt, 256), 256, 0, st>>>(cnt, node, X, x);
+  launch_pdl(k_scatter_add, dim3(ceil_div(3 * (int64_t)cnt, 256)), dim3(256), 0, st, cnt, node, X, x);
 }
 
 void launch_gather3(cudaStream_t st, int cnt, const int* idx, const double* src, double* out) {
