@@ -544,6 +544,11 @@ static bool marker_on(int k) {
 }
 
 int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
+  struct PdlScope {  // concurrent scenes (aux_overlap off): no programmatic launches
+    bool prev;
+    explicit PdlScope(bool off) : prev(tl_pdl_off) { tl_pdl_off = prev || off; }
+    ~PdlScope() { tl_pdl_off = prev; }
+  } pdl_scope(!aux_overlap);
   int launches = 0;
   const ProxyDev P_ = px();
   bool first_detection_done = false;
