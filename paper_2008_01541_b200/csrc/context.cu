@@ -607,17 +607,22 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
         // (4.2) local step on E_beta fused with the beta element forces
         launch_local_forces(st, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
       }
+      // the factorization's flags, counter and backward-chain rows: reset on
+      // the aux stream in the first pass (joined through ev_pre), else here,
+      // ahead of build_g, so build_g -> Cholesky -> dense backward stay
+      // kernel-to-kernel (programmatic launches; ordinary ones under the
+      // concurrent-scene PDL scope)
+      if (!(pre && it == 0)) {
+        SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
+        SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
+        dense_backward_preset(st, dd, xrows.p);
+      }
       // (4.4) g = f~2 + f_beta + f_col, packed as the RHS tile row
       launch_build_g(st, n2, f_tilde2.p, gb_ptr.p, gb_src.p, Gb.p, nbeta, P_, tets.p, x.p, active.p, target.p,
                      gc_ptr.p, gc_src.p, g.p, Y.p);
       // (4.3)+(4.5) H = sigma0 + C22, LL^T = H, y = L^-1 g (one persistent launch), u2 = L^-T y
-      const bool preset = pre && it == 0;  // reset on the aux stream (joined through ev_pre)
-      if (!preset) {
-        SPB_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * (dense_tile_count(N) + N), st));
-        SPB_CUDA(cudaMemsetAsync(counter.p, 0, sizeof(int), st));
-      }
-      launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid, preset);
-      launch_dense_backward(st, dd, xrows.p, u2.p, nullptr, preset);
+      launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid, true);
+      launch_dense_backward(st, dd, xrows.p, u2.p, nullptr, true);
       // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual.
       // In the last pass nothing downstream of the backward sweep needs f~2:
       // u2_accum is updated on the main stream (it feeds the sweep) and the
