@@ -1042,6 +1042,7 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
   const int j = N - 1 - blockIdx.x;
   const int tid = threadIdx.x;
   const int c = tid & 63, grp = tid >> 6;  // 4 groups x 64 columns
+  if (tid == 0) pdl_trigger();  // the u2 consumer behind may launch (it waits for this grid)
   if (await_flags) {
     // launched programmatically behind the factorization: column j of L,
     // inv(L_jj)^T and y_j are read only once their flags are released

@@ -193,6 +193,8 @@ void launch_inner_update(cudaStream_t st, int m, const double* u2, const double*
 // a second stream: u2acc += u2 (the same single add), XF's x2 rows = u2acc.
 __global__ void k_u2acc_to_xf(int m3, const double* __restrict__ u2, double* __restrict__ u2acc,
                               double* __restrict__ xf2) {
+  if (threadIdx.x == 0) pdl_trigger();  // the backward sweep's first launch may follow
+  pdl_wait();                           // u2 of the dense backward
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= m3) return;
   const double v = u2acc[k] + u2[k];
@@ -202,7 +204,7 @@ __global__ void k_u2acc_to_xf(int m3, const double* __restrict__ u2, double* __r
 
 void launch_u2acc_to_xf(cudaStream_t st, int m, const double* u2, double* u2acc, double* xf2) {
   if (m <= 0) return;
-  k_u2acc_to_xf<<<ceil_div(3 * (int64_t)m, 256), 256, 0, st>>>(3 * m, u2, u2acc, xf2);
+  launch_pdl(k_u2acc_to_xf, dim3(ceil_div(3 * (int64_t)m, 256)), dim3(256), 0, st, 3 * m, u2, u2acc, xf2);
 }
 
 void launch_scatter_add(cudaStream_t st, int cnt, const int* node, const double* X, double* x) {
