@@ -233,7 +233,10 @@ __device__ __forceinline__ void element_forces(const double F[9], const double R
 
 // One thread per element of the subset: R (and Q) <- polar(F), and the
 // per-element node forces G (SoA: G[(slot*3+d)*nsub + i]).
-__global__ void __launch_bounds__(128) k_local_forces(int nsub, const int* __restrict__ sub,
+// 6 CTAs per SM (80 registers, a small L1-resident spill): the Jacobi SVD is
+// FP64-latency bound, and 24 instead of 16 resident warps per SM take the
+// alpha step from ~195 to ~186 us at cfg3 (alternated A/B, tools/lib_ab.sh)
+__global__ void __launch_bounds__(128, 6) k_local_forces(int nsub, const int* __restrict__ sub,
                                                       const int4* __restrict__ tets, const double* __restrict__ x,
                                                       const double* __restrict__ dmi,
                                                       const double* __restrict__ vol, int64_t ne,
