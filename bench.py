@@ -40,8 +40,20 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
 
-# BASELINE.json's metric, verbatim (both arms print it)
+# BASELINE.json's metric, verbatim, for its headline config 3 (both arms print
+# it); the other single-scene configs state their own size in the same form
 METRIC = "PD frames/sec w/ collisions at 600K tets, 5% collision DOFs; Cholesky FP64 TFLOPS"
+METRICS = {
+    "cfg3": METRIC,
+    "cfg2": "PD frames/sec w/ collisions at 100K tets, 5% collision DOFs (BASELINE config 2); Cholesky FP64 TFLOPS",
+    "cfg5": "PD frames/sec w/ collisions, one 150K-tet scene, 5% collision DOFs (BASELINE config 5 scene); "
+            "Cholesky FP64 TFLOPS",
+    "cfg1": "PD frames/sec w/ collisions, 6.4K-tet beam, 5% collision DOFs (BASELINE config 1); Cholesky FP64 TFLOPS",
+}
+
+
+def metric_for(config: str) -> str:
+    return METRICS.get(config, METRIC)
 
 
 def _env_rank():
@@ -135,21 +147,27 @@ def measured_hbm_peak():
         return 6552.3, "fallback (no MEASURED_PEAKS.json on this box)"
 
 
-def committed_traffic():
+def committed_traffic(config: str, m: int):
     """dram__bytes_read.sum + dram__bytes_write.sum of one k_cholesky_tiles
-    launch from the newest committed `ncu --set full` capture (profiles/)."""
-    caps = sorted((ROOT / "profiles").glob("r*_cholesky_traffic.json"))
-    if not caps:
-        return None, None
-    js = json.loads(caps[-1].read_text())
-    return js.get("traffic_bytes"), f"profiles/{caps[-1].name} (ncu --set full, one launch)"
+    launch of THIS config (dense order m) from the newest committed
+    `ncu --set full` capture (profiles/r*_cholesky_traffic_<config>.json);
+    None when no capture of this config is committed."""
+    caps = sorted((ROOT / "profiles").glob(f"r*_cholesky_traffic_{config}.json"))
+    if config == "cfg3":
+        caps = sorted(caps + sorted((ROOT / "profiles").glob("r01_cholesky_traffic.json")))
+    for cap in reversed(caps):
+        js = json.loads(cap.read_text())
+        if int(js.get("m", m)) == m:
+            return js.get("traffic_bytes"), f"profiles/{cap.name} (ncu --set full, one launch)"
+    return None, None
 
 
-def build_sim(config: str, outer: int, inner: int):
+def build_sim(config: str, outer: int, inner: int, collider: str = "plane"):
     import paper_2008_01541_b200 as P
     from scenes import config_yaml
 
-    text = config_yaml(config, outer=outer, inner=inner) if config != "cfg1" else config_yaml(config)
+    text = (config_yaml(config, outer=outer, inner=inner, collider=collider) if config != "cfg1"
+            else config_yaml(config))
     sc = P.parse_scenario(text)
     t0 = time.perf_counter()
     sim = P.Simulation(sc, diagnostics=False)
@@ -196,43 +214,126 @@ def cpu_oracle_frames(sim, frames: int, threads: int):
     return float(np.median(times)), times
 
 
+def _ref_scene_yaml(args) -> str:
+    """The workload's scenario YAML without importing this package (the
+    reference arm must not load it): tests/scene_yaml.py templates."""
+    from scene_yaml import CONFIGS, block_yaml
+
+    if args.config == "cfg1":
+        return str(np.load(ROOT / "tests" / "golden" / "cfg1.npz")["yaml"])
+    return block_yaml(*CONFIGS[args.config], outer=args.outer, inner=args.inner, collider=args.collider)
+
+
 def run_reference(args):
+    """The reference arm: the UNMODIFIED reference package (`schurpd`,
+    installed into baseline/_ref from /root/reference) through its own public
+    API, `harness.Simulation(parse_scenario(yaml)).step()` (harness.py:592-596),
+    on this host's cores. The scene (same YAML as our arm), the precompute
+    (`build_system`: AMD + scalar partial Cholesky, ~8 min at cfg3) and the
+    warm-up run outside the timed region; then exactly the timed frames are
+    stepped. This process never imports paper_2008_01541_b200. Falls back to
+    the oracle port (oracle/oracle.py) only when baseline/_ref is absent."""
     rank, world, _ = _env_rank()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(threads))
-    sim, setup_s = build_sim(args.config, args.outer, args.inner)
-    for _ in range(args.warmup):
-        pass
-    # bounded sample: at most --ref-frames frames of the workload (the oracle
-    # takes ~1.5 s per 600K frame on 16 cores), reported as frames/s
+    cores = os.cpu_count() or 1
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "schurpd" / "__init__.py").exists():
+        return run_reference_port(args)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/spb_numba_cache")
+    sys.path.insert(0, str(ref))
+    from threadpoolctl import threadpool_limits
+
+    from schurpd import harness as RH  # the stock reference
+
+    assert "paper_2008_01541_b200" not in sys.modules
+    t0 = time.perf_counter()
+    sim = RH.Simulation(RH.parse_scenario(_ref_scene_yaml(args)))
+    setup_s = time.perf_counter() - t0
+    # warm-up (numba JIT, first touch) doubles as the OpenBLAS thread sweep:
+    # numpy and scipy each spin an OpenBLAS pool, so "all cores" can be slower
+    # than fewer (BASELINE.md §2); the best setting is then used for timing
+    cands = sorted({1, max(1, cores // 2), cores})
+    tried = {}
+    for w in range(max(args.warmup, len(cands) + 1)):
+        th = cands[(w - 1) % len(cands)] if w >= 1 else cores
+        with threadpool_limits(limits=th):
+            t1 = time.perf_counter()
+            sim.step()
+            dt = time.perf_counter() - t1
+        if w >= 1:
+            tried[th] = min(dt, tried.get(th, 1e30))
+    best = min(tried, key=tried.get)
     nf = max(1, min(args.steps, args.ref_frames))
-    sec, times = cpu_oracle_frames(sim, nf, threads)
+    times = []
+    with threadpool_limits(limits=best):
+        for _ in range(nf):
+            t1 = time.perf_counter()
+            sim.step()
+            times.append(time.perf_counter() - t1)
+    sec = float(np.mean(times))
     value = 1.0 / sec
+    m = sim.partition.n2
     line = {
-        "impl": "reference", "metric": METRIC,
-        "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "metric": metric_for(args.config),
+        "value": value, "unit": "frames/s", "n_gpus": args.gpus, "steps": nf, "warmup": args.warmup,
         "ms_per_step": 1e3 * sec, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": _config_dict(sim, args),
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{len(times)} frames of {args.config} (oracle/oracle.py, OR_THREADS={threads}, "
-                                   f"OpenBLAS threads {os.environ.get('OPENBLAS_NUM_THREADS')})"},
+        "dtype": "f64", "data": "synthetic (lattice scene through the reference schema)",
+        "config": {"workload": f"{args.config}: {sim.mesh.num_elements} tets, {sim.mesh.num_nodes} nodes, "
+                               f"m={m} prone ({100.0 * m / sim.mesh.num_nodes:.2f}%), "
+                               f"{len(sim.model.proxies)} proxies, collider {args.collider}",
+                   "outer_iters": args.outer, "inner_iters": args.inner,
+                   "parallelism": "host CPU (reference runs one frame on one logical thread + BLAS pools)"},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": best, "kind": "reference",
+                         "sample": f"{nf} frames of {args.config} through the stock reference "
+                                   f"(baseline/_ref schurpd, Simulation.step), mean {sec:.3f} s/frame; "
+                                   f"OpenBLAS threads {best} (best of {sorted(tried)} on {cores} host cores: "
+                                   + ", ".join(f"{k}: {v:.2f} s" for k, v in sorted(tried.items())) + ")"},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_s": setup_s,
     }
     print(json.dumps(line), flush=True)
 
 
+def run_reference_port(args):
+    """Fallback when the reference is not installed: the oracle port
+    (oracle/oracle.py, the reference algorithm restated on numpy/scipy + C)."""
+    threads = os.cpu_count() or 1
+    sim, setup_s = build_sim(args.config, args.outer, args.inner, args.collider)
+    nf = max(1, min(args.steps, args.ref_frames))
+    sec, times = cpu_oracle_frames(sim, nf, threads)
+    value = 1.0 / sec
+    print(json.dumps({
+        "impl": "reference", "metric": metric_for(args.config), "value": value, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": len(times), "warmup": 0, "ms_per_step": 1e3 * sec, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(sim, args),
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{len(times)} frames of {args.config} (oracle/oracle.py; baseline/_ref absent)"},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+        flush=True)
+
+
+L2_BYTES = 126 * 2 ** 20  # B200 L2
+
+
 def _config_dict(sim, args):
     f = sim.system.factor.native
+    m = f.n2
+    panels = 8.0 * f.panel_values
+    tri = 8.0 * m * (m + 1) / 2
+    per_frame = 2 * panels + 2 * tri
+    l2 = (f"inputs larger than L2 ({panels / 1e6:.0f} MB supernodal panels read twice + {tri / 1e6:.0f} MB "
+          f"sigma0 tiles in, {tri / 1e6:.0f} MB L out per frame vs {L2_BYTES / 2 ** 20:.0f} MB L2)"
+          if per_frame > L2_BYTES else
+          f"per-frame working set {per_frame / 1e6:.0f} MB fits the {L2_BYTES / 2 ** 20:.0f} MB L2: frames are "
+          f"timed back to back without a flush (steady-state replay, L2-warm)")
     return {"workload": f"{args.config}: {sim.mesh.num_elements} tets, {sim.mesh.num_nodes} nodes, "
                         f"m={sim.partition.n2} prone ({100.0 * sim.partition.n2 / sim.mesh.num_nodes:.2f}%), "
-                        f"{len(sim.model.proxies)} proxies",
+                        f"{len(sim.model.proxies)} proxies, collider {args.collider}",
             "outer_iters": args.outer, "inner_iters": args.inner, "n1": f.n1, "m": f.n2,
             "nnz_L1": f.nnz_l1, "nnz_C": f.nnz_c, "supernodes": f.nsuper, "tree_levels": f.levels,
-            "l2": "inputs larger than L2 (613 MB supernodal panels + 154 MB sigma0 tiles per frame at cfg3)",
-            "parallelism": f"replicas x{args.gpus} (independent scene per GPU)"}
+            "l2": l2, "parallelism": f"replicas x{args.gpus} (independent scene per GPU, no collective)"}
 
 
 def run_b200(args):
@@ -249,14 +350,17 @@ def run_b200(args):
         import torch.distributed as dist_mod
 
         torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl")
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
-    os.environ.setdefault("CUDA_VISIBLE_DEVICES", os.environ.get("CUDA_VISIBLE_DEVICES", ""))
-    sim, setup_s = build_sim(args.config, args.outer, args.inner)
+    sim, setup_s = build_sim(args.config, args.outer, args.inner, args.collider)
     # warm-up through the public API (also captures the CUDA graph)
     for _ in range(args.warmup):
         sim.step()
     ds = device_scene(sim.model, sim.system)
+    dev_ids = [ds.device]
+    if dist is not None:  # which GPU each rank's scene lives on (one per rank)
+        dev_ids = [None] * world
+        dist.all_gather_object(dev_ids, ds.device)
     cfg = _native.StepConfig(args.outer, args.inner, _native.CADENCES[sim.config.detection_cadence], 1, 0, -1.0)
     lib = _native.lib()
 
@@ -296,7 +400,7 @@ def run_b200(args):
             dist.destroy_process_group()
         return
     fp64_peak = measure_fp64_peak()
-    traffic, traffic_src = committed_traffic()
+    traffic, traffic_src = committed_traffic(args.config, m)
     # per-piece graph-replay times -> achieved HBM GB/s of the solves (north_star (4))
     kms = {}
     for name, which in (("cholesky", 0), ("dense_backward", 1), ("sigma0_gemv", 2), ("sparse_forward", 3),
@@ -315,7 +419,7 @@ def run_b200(args):
     t_hbm = bytes_frame / (hbm_peak * 1e9) * 1e3
     achieved = chol_flops / (chol.value * 1e-3) / 1e12
     line = {
-        "metric": METRIC,
+        "metric": metric_for(args.config),
         "value": replica_throughput(world, ms_frame), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_frame, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (lattice scene through the reference schema)",
@@ -340,7 +444,7 @@ def run_b200(args):
                            "t_roofline_ms": t_fp64 + t_hbm, "frac": (t_fp64 + t_hbm) / ms_frame,
                            "note": "m^3/3 at the live DGEMM peak + algorithmic bytes (2 sweeps of panels, "
                                    "4 triangle passes, element and metric passes) at the HBM peak"},
-        "gpu_launches": launches, "setup_s": setup_s,
+        "gpu_launches": launches, "setup_s": setup_s, "device_ids": dev_ids, "gpus_active": len(set(dev_ids)),
         "clocks": clk.summary(),
     }
     if world == 1:
@@ -407,7 +511,7 @@ def run_batch(args):
         import torch.distributed as dist_mod
 
         torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl")
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
     S = args.scenes
     t0 = time.perf_counter()
@@ -494,7 +598,7 @@ def run_dense(args):
         import torch.distributed as dist_mod
 
         torch.cuda.set_device(local)
-        dist_mod.init_process_group("nccl")
+        dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = dist_mod
     sizes = [int(v) for v in args.sizes.split(",")] if args.sizes else list(CFG4_SIZES)
     clk = ClockSampler(local)
@@ -637,6 +741,40 @@ def met_launches(ds, cfg):
     return met.kernel_launches
 
 
+def probe_ranks():
+    """Launcher self-check: each rank joins a gloo group, resolves the device
+    its scenes would be created on (_native.default_device: LOCAL_RANK) and
+    rank 0 prints them all (tests/test_replicas.py)."""
+    import torch.distributed as dist_mod
+
+    from paper_2008_01541_b200 import _native
+
+    rank, world, local = _env_rank()
+    dist_mod.init_process_group("gloo")
+    dev = _native.default_device()
+    got = [None] * world
+    dist_mod.all_gather_object(got, {"rank": rank, "local_rank": local, "device": dev})
+    if rank == 0:
+        print(json.dumps({"world": world, "ranks": got}), flush=True)
+    dist_mod.destroy_process_group()
+
+
+def spawn_cmd(n: int, argv, port: int):
+    """`bench.py --gpus N` run directly: one process per GPU under torchrun
+    (the layout the driver launches), rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *argv]
+
+
+def spawn_ranks(n: int) -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    return subprocess.call(spawn_cmd(n, sys.argv[1:], port))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -647,7 +785,12 @@ def main():
     ap.add_argument("--outer", type=int, default=1)
     ap.add_argument("--inner", type=int, default=1)
     ap.add_argument("--cpu-frames", type=int, default=3)
-    ap.add_argument("--ref-frames", type=int, default=8)
+    ap.add_argument("--probe-ranks", action="store_true",
+                    help="launcher self-check (CPU, gloo): every rank prints its rank and scene device")
+    ap.add_argument("--ref-frames", type=int, default=20, help="reference arm: cap on timed frames")
+    ap.add_argument("--collider", default="plane", choices=["plane", "jaw"],
+                    help="cfg2/3/5: half-space pressing down, or 'jaw' (capsule on a rotate motion: the "
+                         "articulated-contact variant BASELINE config 3 names)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--scenes", type=int, default=1, help="batch mode: concurrent scenes per GPU (cfg5)")
     ap.add_argument("--sizes", default="", help="cfg4: comma-separated dense orders (default 2048..49152)")
@@ -655,7 +798,11 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference" and args.config == "cfg4":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.probe_ranks:
+        probe_ranks()
+    elif args.impl == "reference" and args.config == "cfg4":
         run_dense_reference(args)
     elif args.impl == "reference":
         run_reference(args)

@@ -74,6 +74,9 @@ typedef struct spb_ctx spb_ctx;
 int32_t spb_version(void);
 const char *spb_last_error(void);
 int32_t spb_device_count(int32_t *count);
+/* The calling thread's current CUDA device (contexts default to it, or to
+ * LOCAL_RANK under torchrun: one process per GPU). */
+int32_t spb_get_device(int32_t *device);
 /* Page-lock a caller-owned host range so spb_ctx_set_state / get_state move
  * it by DMA without staging (e.g. a SolverState.x reused every frame); the
  * caller unregisters it before freeing the memory. */
@@ -176,6 +179,7 @@ typedef struct {
   double max_penetration, residual;
   int64_t info;               /* failing column on SPB_ERR_INDEFINITE */
   int64_t kernel_launches;    /* kernels this step launched */
+  int64_t outer_passes;       /* outer passes run (< outer_iters after an early exit, solver.py:448-452) */
 } spb_frame_metrics;
 
 int32_t spb_ctx_create(const spb_scene_desc *scene, const spb_factor *factor, int32_t device, spb_ctx **out);

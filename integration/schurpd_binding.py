@@ -70,7 +70,8 @@ class StepConfig(ctypes.Structure):  # spb_step_config
 class Metrics(ctypes.Structure):  # spb_frame_metrics
     _fields_ = [("t_local_ms", F64), ("t_forward_ms", F64), ("t_detect_ms", F64), ("t_dense_ms", F64),
                 ("t_backward_ms", F64), ("t_total_ms", F64), ("energy", F64), ("active_proxies", I64),
-                ("max_penetration", F64), ("residual", F64), ("info", I64), ("kernel_launches", I64)]
+                ("max_penetration", F64), ("residual", F64), ("info", I64), ("kernel_launches", I64),
+                ("outer_passes", I64)]
 
 
 _lib = None

@@ -9,8 +9,8 @@ missing, calls raise instead of computing anything on the host.
 from __future__ import annotations
 
 import ctypes
-import weakref
 import os
+import weakref
 import subprocess
 from pathlib import Path
 from typing import Optional, Sequence
@@ -73,13 +73,15 @@ class FrameIO(ctypes.Structure):
 class FrameMetricsC(ctypes.Structure):
     _fields_ = [("t_local_ms", F64), ("t_forward_ms", F64), ("t_detect_ms", F64), ("t_dense_ms", F64),
                 ("t_backward_ms", F64), ("t_total_ms", F64), ("energy", F64), ("active_proxies", I64),
-                ("max_penetration", F64), ("residual", F64), ("info", I64), ("kernel_launches", I64)]
+                ("max_penetration", F64), ("residual", F64), ("info", I64), ("kernel_launches", I64),
+                ("outer_passes", I64)]
 
 
 _SIGS = {
     "spb_version": ([], I32),
     "spb_last_error": ([], ctypes.c_char_p),
     "spb_device_count": ([P], I32),
+    "spb_get_device": ([P], I32),
     "spb_host_register": ([P, I64], I32),
     "spb_host_unregister": ([P], I32),
     "spb_set_host_blas": ([P, P, P, P, P], I32),
@@ -265,6 +267,20 @@ def device_count() -> int:
     c = ctypes.c_int32(0)
     rc = lib().spb_device_count(ctypes.byref(c))
     return int(c.value) if rc == SPB_OK else 0
+
+
+def default_device() -> int:
+    """The GPU this process drives: SPB_DEVICE, else LOCAL_RANK (torchrun: one
+    process per GPU; folded onto the visible devices when a launcher already
+    restricted CUDA_VISIBLE_DEVICES per rank), else the current CUDA device."""
+    for var in ("SPB_DEVICE", "LOCAL_RANK"):
+        v = os.environ.get(var)
+        if v not in (None, ""):
+            n = device_count()
+            d = int(v)
+            return d if d < n or n == 0 else d % n
+    c = ctypes.c_int32(0)
+    return int(c.value) if lib().spb_get_device(ctypes.byref(c)) == SPB_OK else 0
 
 
 def require_device() -> None:

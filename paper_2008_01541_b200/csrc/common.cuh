@@ -30,6 +30,27 @@ constexpr int NUM_SMS_B200 = 148;
     }                                                                                   \
   } while (0)
 
+// ------------------------------------------------------------ bounded spins
+// Every inter-CTA / inter-GPU wait (tile flags, solved-row sentinels, grid
+// barriers, dataflow counters) is bounded in TIME: a wait longer than
+// kSpinLimitNs (a dead peer GPU, a lost flag) traps, which fails the launch
+// with an error instead of leaving the device hung. The clock is read only
+// every 64th spin, so a flag that is already set costs nothing extra.
+constexpr unsigned long long kSpinLimitNs = 60ull * 1000ull * 1000ull * 1000ull;  // 60 s
+
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  unsigned it = 0;
+  __device__ __forceinline__ void tick() {
+    if ((++it & 63u) == 0u) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > kSpinLimitNs) __trap();
+    }
+  }
+};
+
 // ------------------------------------------------------------ collider data
 struct ShapeDev {
   int kind;

@@ -163,6 +163,9 @@ struct Ctx {
   DBuf<int> pcg_iters, pcg_track;
   int* pcg_host = nullptr;           // pinned: track[2] (max iterations, error iteration)
   double* pcg_resid_host = nullptr;  // pinned: [3]
+  DBuf<double> eq_sumsq;             // early exit: sum of squared pose forces
+  double* eq_host = nullptr;         // pinned
+  int outer_passes = 0;              // outer passes the last frame ran
   // graph cache
   std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>> graphs;  // solve, metrics
   int last_launches = 0;
@@ -183,6 +186,7 @@ struct Ctx {
     if (metrics_host) cudaFreeHost(metrics_host);
     if (pcg_host) cudaFreeHost(pcg_host);
     if (pcg_resid_host) cudaFreeHost(pcg_resid_host);
+    if (eq_host) cudaFreeHost(eq_host);
     if (ev_state) cudaEventDestroy(ev_state);
     if (st_io) cudaStreamDestroy(st_io);
     if (st_aux) cudaStreamDestroy(st_aux);
@@ -200,8 +204,11 @@ struct Ctx {
   int enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev /* 6 phase events or null */);
   int enqueue_metrics(cudaEvent_t* ev);
   int build_pcg(int64_t nrows, const int64_t* Ap, const int64_t* Ai, const double* Ax);
-  int enqueue_pcg(int outer, int inner, int cadence, double tol, int max_iters);
+  int enqueue_pcg(int outer, int inner, int cadence, double tol, int max_iters, bool reset_track);
   int sync_shapes();
+  void drop_graphs();
+  int ensure_pose_gather();
+  int enqueue_equilibrium_residual();
   int io_reserve(size_t bytes) {
     if (bytes <= io_bytes) return SPB_OK;
     if (io_host) cudaFreeHost(io_host);
@@ -373,8 +380,8 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   TRY(XF.zeros(3 * (size_t)n));
   if (n1 > 0) {
     TRY(build_device_factor(*f));
-    TRY(U.zeros(3 * std::max<size_t>(device_factor_ubuf(*f->dev), 1)));
-    TRY(sweep_work_alloc(*f->dev, sw));
+    TRY(U.zeros(3 * std::max<size_t>(device_factor_ubuf(*f->dev_on(device)), 1)));
+    TRY(sweep_work_alloc(*f->dev_on(device), sw));
   }
   // beta gather (trailing-local keys) and proxies
   std::vector<int> key2(n, -1);
@@ -507,11 +514,32 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   return SPB_OK;
 }
 
+// Shape records live in a device array whose ADDRESS is baked into every
+// captured graph (k_detect, k_proxy_final). New shapes (e.g. a collider with
+// active_from_frame > 0 registered after graphs exist) are written in place;
+// only when the capacity must grow is the array reallocated, and then every
+// captured graph is dropped first so no graph keeps the freed pointer.
 int Ctx::sync_shapes() {
   if (!shapes_dirty) return SPB_OK;
-  TRY(shapes_dev.upload(shapes.data(), shapes.size()));
+  if (shapes.size() > shapes_dev.n || !shapes_dev.p) {
+    SPB_CUDA(cudaStreamSynchronize(st));
+    drop_graphs();
+    TRY(shapes_dev.alloc(std::max<size_t>(16, 2 * shapes.size())));
+  }
+  if (!shapes.empty())
+    SPB_CUDA(cudaMemcpyAsync(shapes_dev.p, shapes.data(), sizeof(spb::ShapeDev) * shapes.size(),
+                             cudaMemcpyHostToDevice, st));
+  SPB_CUDA(cudaStreamSynchronize(st));  // the host vector may grow (reallocate) before the next call
   shapes_dirty = false;
   return SPB_OK;
+}
+
+void Ctx::drop_graphs() {
+  for (auto& kv : graphs) {
+    cudaGraphExecDestroy(kv.second.first);
+    cudaGraphExecDestroy(kv.second.second);
+  }
+  graphs.clear();
 }
 
 // The frame: solve_frame_schur (solver.py:387-455) + _finish_metrics (:373-384).
@@ -586,7 +614,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
     if (ev && o == outer - 1) SPB_CUDA(mark_phase(ev, 1, st));
     // (3) forward substitution: y1 = L1^-1 f1[fill], f~2 = f2 - C y1
     if (n1 > 0) {
-      sparse_forward(st, *factor->dev, b.p, y.p, U.p, f_tilde2.p, &launches, &sw);
+      sparse_forward(st, *factor->dev_on(device), b.p, y.p, U.p, f_tilde2.p, &launches, &sw);
     } else if (n2 > 0) {
       SPB_CUDA(cudaMemcpyAsync(f_tilde2.p, b.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice, st));
     }
@@ -652,7 +680,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       if (n2 > 0 && !aux_pending)
         SPB_CUDA(cudaMemcpyAsync(XF.p + 3 * (size_t)n1, u2acc.p, sizeof(double) * 3 * n2, cudaMemcpyDeviceToDevice,
                                  st));
-      sparse_backward(st, *factor->dev, y.p, XF.p, &launches, &sw);
+      sparse_backward(st, *factor->dev_on(device), y.p, XF.p, &launches, &sw);
       launch_scatter_add(st, n1, x1_node.p, XF.p, x.p);
       launches++;
     }
@@ -663,6 +691,63 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
     if (ev && o == outer - 1) SPB_CUDA(mark_phase(ev, 4, st));
   }
   last_launches = launches;
+  return SPB_OK;
+}
+
+// ------------------------------------------------- pose forces (all elements)
+// reference _pose_forces (solver.py:468-481): every element's elastic force at
+// the current x / R (/ Q), the attachment springs, then the collision forces
+// of the current active set; gathered per node in factor order, deterministic.
+int Ctx::ensure_pose_gather() {
+  if (gall_ptr.p) return SPB_OK;
+  std::vector<int> key_of_node(n);
+  for (int64_t k = 0; k < n; ++k) key_of_node[fac_h[k]] = (int)k;
+  std::vector<int4> t4(ne);
+  SPB_CUDA(cudaMemcpy(t4.data(), tets.p, sizeof(int4) * ne, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> th(4 * ne);
+  for (int64_t e = 0; e < ne; ++e) {
+    th[4 * e] = t4[e].x; th[4 * e + 1] = t4[e].y; th[4 * e + 2] = t4[e].z; th[4 * e + 3] = t4[e].w;
+  }
+  Csr ga = element_gather(th, nullptr, ne, key_of_node, (int)n);
+  TRY(gall_ptr.upload(ga.ptr));
+  TRY(gall_src.upload(ga.src));
+  TRY(Gall.alloc(12 * (size_t)ne));
+  TRY(zeros_n2.zeros((size_t)n2 + 1));
+  TRY(eq_sumsq.zeros(1));
+  if (!eq_host) SPB_CUDA(cudaMallocHost(&eq_host, sizeof(double)));
+  return SPB_OK;
+}
+
+// sum of squares of v[0 .. cnt) in one block, fixed order (bit-reproducible)
+__global__ void __launch_bounds__(1024) k_sumsq(const double* __restrict__ v, int64_t cnt,
+                                                double* __restrict__ out) {
+  __shared__ double part[32];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) a = fma(v[i], v[i], a);
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    a = part[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) out[0] = a;
+  }
+}
+
+// RMS of the total nodal force into eq_host (reference _equilibrium_residual,
+// solver.py:468-471); the pose forces land in b (factor order). No sync.
+int Ctx::enqueue_equilibrium_residual() {
+  const ProxyDev P_ = px();
+  launch_local_forces(st, (int)ne, nullptr, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gall.p, 0);
+  launch_gather_forces(st, (int)n, gall_ptr.p, gall_src.p, Gall.p, (int)ne, fac_node.p, att_ptr.p, att_idx.p,
+                       att_k.p, att_tgt.p, x.p, b.p);
+  if (n2 > 0)
+    launch_build_g(st, n2, b.p + 3 * (size_t)n1, zeros_n2.p, zeros_n2.p, Gall.p, 1, P_, tets.p, x.p, active.p,
+                   target.p, gc_ptr.p, gc_src.p, b.p + 3 * (size_t)n1, nullptr);
+  k_sumsq<<<1, 1024, 0, st>>>(b.p, 3 * n, eq_sumsq.p);
+  SPB_CUDA(cudaGetLastError());
+  SPB_CUDA(cudaMemcpyAsync(eq_host, eq_sumsq.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  last_launches += 3 + (n2 > 0);
   return SPB_OK;
 }
 
@@ -744,18 +829,7 @@ int Ctx::build_pcg(int64_t nrows, const int64_t* Ap, const int64_t* Ai, const do
   TRY(pcg_bar.zeros(1));
   TRY(pcg_iters.zeros(4));
   TRY(pcg_track.zeros(2));
-  TRY(zeros_n2.zeros((size_t)n2 + 1));
-  // all-element node gather in factor order (reference _pose_forces: every element)
-  std::vector<int4> t4(ne);
-  SPB_CUDA(cudaMemcpy(t4.data(), tets.p, sizeof(int4) * ne, cudaMemcpyDeviceToHost));
-  std::vector<int64_t> th(4 * ne);
-  for (int64_t e = 0; e < ne; ++e) {
-    th[4 * e] = t4[e].x; th[4 * e + 1] = t4[e].y; th[4 * e + 2] = t4[e].z; th[4 * e + 3] = t4[e].w;
-  }
-  Csr ga = element_gather(th, nullptr, ne, key_of_node, (int)n);
-  TRY(gall_ptr.upload(ga.ptr));
-  TRY(gall_src.upload(ga.src));
-  TRY(Gall.alloc(12 * (size_t)ne));
+  TRY(ensure_pose_gather());
   if (!pcg_host) SPB_CUDA(cudaMallocHost(&pcg_host, sizeof(int) * 4));
   if (!pcg_resid_host) SPB_CUDA(cudaMallocHost(&pcg_resid_host, sizeof(double) * 3));
   SPB_CUDA(cudaDeviceSynchronize());
@@ -771,13 +845,13 @@ __global__ void k_pcg_track(const int* __restrict__ iters, int* __restrict__ tra
 }
 
 // solve_frame_pcg (reference solver.py:542-603), one device enqueue per frame
-int Ctx::enqueue_pcg(int outer, int inner, int cadence, double tol, int max_iters) {
+int Ctx::enqueue_pcg(int outer, int inner, int cadence, double tol, int max_iters, bool reset_track) {
   if (!have_pcg) { set_error("PCG needs the operator (spb_ctx_set_operator)"); return SPB_ERR_ARG; }
   int launches = 0;
   const ProxyDev P_ = px();
   bool first_detection_done = false;
   residual_valid = false;
-  SPB_CUDA(cudaMemsetAsync(pcg_track.p, 0, sizeof(int) * 2, st));
+  if (reset_track) SPB_CUDA(cudaMemsetAsync(pcg_track.p, 0, sizeof(int) * 2, st));
   SPB_CUDA(cudaMemsetAsync(pcg_resid.p, 0, sizeof(double) * 3, st));
   double* V = pcg_vec.p;
   const size_t n3 = 3 * (size_t)n;
@@ -870,6 +944,18 @@ int32_t spb_device_count(int32_t* count) {
     return SPB_ERR_CUDA;
   }
   *count = c;
+  return SPB_OK;
+}
+
+int32_t spb_get_device(int32_t* device) {
+  int d = 0;
+  cudaError_t e = cudaGetDevice(&d);
+  if (e != cudaSuccess) {
+    *device = 0;
+    spb::set_error(std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+    return SPB_ERR_CUDA;
+  }
+  *device = d;
   return SPB_OK;
 }
 
@@ -1026,9 +1112,36 @@ static int ensure_graphs(Ctx* c, const spb_step_config* cfg,
   return SPB_OK;
 }
 
+// Early exit (solver.py:448-452): after every outer pass the RMS of the total
+// nodal force (_equilibrium_residual, :468-471) is computed on the device and
+// read back; the remaining passes are skipped once it is <= the threshold.
+// 'frame' cadence detects only in the first pass (first_detection_done
+// persists across passes, :417-421), so later passes run as 'never'.
+static int run_frame_early_exit(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
+  TRY(c->ensure_pose_gather());
+  c->last_graph = false;
+  int launches = 0;
+  c->outer_passes = 0;
+  for (int o = 0; o < cfg->outer_iters; ++o) {
+    const int cad = (o > 0 && cfg->cadence == SPB_CADENCE_FRAME) ? SPB_CADENCE_NEVER : cfg->cadence;
+    TRY(c->enqueue_solve(1, cfg->inner_iters, cad, ev));
+    TRY(c->enqueue_equilibrium_residual());
+    launches += c->last_launches;
+    SPB_CUDA(cudaStreamSynchronize(c->st));
+    c->outer_passes = o + 1;
+    const double rms = std::sqrt(*c->eq_host / (3.0 * (double)c->n));
+    if (rms <= cfg->early_exit_residual) break;
+  }
+  SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
+  c->last_launches = launches;
+  return c->enqueue_metrics(ev);
+}
+
 static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
   const int outer = cfg->outer_iters, inner = cfg->inner_iters, cad = cfg->cadence;
   TRY(c->sync_shapes());
+  if (cfg->early_exit_residual >= 0.0) return run_frame_early_exit(c, cfg, ev);
+  c->outer_passes = outer;
   if (cfg->use_graph && !ev) {
     std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>::iterator it;
     TRY(ensure_graphs(c, cfg, &it));
@@ -1072,6 +1185,7 @@ static int frame_finish(Ctx* c, spb_frame_metrics* m) {
   m->residual = c->residual_valid ? c->metrics_host[2] : 0.0;
   m->active_proxies = (int64_t)llround(c->metrics_host[3]);
   m->kernel_launches = c->last_launches;
+  m->outer_passes = c->outer_passes;
   const int info_h = *reinterpret_cast<const int*>(c->metrics_host + 4);
   if (info_h > 0) {
     m->info = info_h - 1;
@@ -1213,7 +1327,24 @@ int32_t spb_ctx_frame_pcg(spb_ctx* cp, const double* att_targets, int32_t ncol, 
   if (c->P) up.add(c->target.p, target, sizeof(double) * 3 * c->P);
   TRY(io_upload(c, up, false));
   TRY(c->sync_shapes());
-  TRY(c->enqueue_pcg(cfg->outer_iters, cfg->inner_iters, cfg->cadence, tol, (int)max_iters));
+  if (cfg->early_exit_residual >= 0.0) {
+    // early exit (solver.py:598-602): device equilibrium residual per outer pass
+    TRY(c->ensure_pose_gather());
+    int launches = 0;
+    for (int o = 0; o < cfg->outer_iters; ++o) {
+      const int cad = (o > 0 && cfg->cadence == SPB_CADENCE_FRAME) ? SPB_CADENCE_NEVER : cfg->cadence;
+      TRY(c->enqueue_pcg(1, cfg->inner_iters, cad, tol, (int)max_iters, o == 0));
+      TRY(c->enqueue_equilibrium_residual());
+      launches += c->last_launches;
+      SPB_CUDA(cudaStreamSynchronize(c->st));
+      c->outer_passes = o + 1;
+      if (std::sqrt(*c->eq_host / (3.0 * (double)c->n)) <= cfg->early_exit_residual) break;
+    }
+    c->last_launches = launches;
+  } else {
+    TRY(c->enqueue_pcg(cfg->outer_iters, cfg->inner_iters, cfg->cadence, tol, (int)max_iters, true));
+    c->outer_passes = cfg->outer_iters;
+  }
   SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
   TRY(c->enqueue_metrics(nullptr));
   SPB_CUDA(cudaMemcpyAsync(c->metrics_host, c->metrics_out.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
@@ -1229,6 +1360,7 @@ int32_t spb_ctx_frame_pcg(spb_ctx* cp, const double* att_targets, int32_t ncol, 
   m->active_proxies = (int64_t)llround(c->metrics_host[3]);
   m->residual = std::max(c->pcg_resid_host[0], std::max(c->pcg_resid_host[1], c->pcg_resid_host[2]));
   m->kernel_launches = c->last_launches;
+  m->outer_passes = c->outer_passes;
   if (pcg_iterations) *pcg_iterations = c->pcg_host[0];
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (c->pcg_host[1] > 0) {
@@ -1323,8 +1455,8 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
       spb::launch_sym_tile_gemv(c->st, c->dd, c->u2.p, c->gemv_partial.p);
       spb::launch_sym_tile_gemv_reduce(c->st, c->dd, c->gemv_partial.p, c->s0u.p);
       break;
-    case 3: spb::sparse_forward(c->st, *c->factor->dev, c->b.p, c->y.p, c->U.p, c->f_tilde2.p, nullptr, &c->sw); break;
-    case 4: spb::sparse_backward(c->st, *c->factor->dev, c->y.p, c->XF.p, nullptr, &c->sw); break;
+    case 3: spb::sparse_forward(c->st, *c->factor->dev_on(c->device), c->b.p, c->y.p, c->U.p, c->f_tilde2.p, nullptr, &c->sw); break;
+    case 4: spb::sparse_backward(c->st, *c->factor->dev_on(c->device), c->y.p, c->XF.p, nullptr, &c->sw); break;
   }
   cudaError_t ce = cudaStreamEndCapture(c->st, &g);
   if (ce != cudaSuccess) { spb::set_error(std::string("capture: ") + cudaGetErrorString(ce)); return SPB_ERR_CUDA; }
@@ -1374,11 +1506,7 @@ int32_t spb_ctx_set_concurrency(spb_ctx* cp, int32_t n) {
   if (g == c->chol_grid && aux == c->aux_overlap) return SPB_OK;
   SPB_CUDA(cudaSetDevice(c->device));
   SPB_CUDA(cudaStreamSynchronize(c->st));
-  for (auto& kv : c->graphs) {
-    cudaGraphExecDestroy(kv.second.first);
-    cudaGraphExecDestroy(kv.second.second);
-  }
-  c->graphs.clear();
+  c->drop_graphs();
   c->chol_grid = g;
   c->aux_overlap = aux;
   return SPB_OK;

@@ -106,12 +106,20 @@ template <bool MULTI = false>
 __device__ __forceinline__ void poll_flag(const int* f, int v) {
   if (MULTI) {
     if (ld_relaxed_sys(f) < v) {
-      while (ld_relaxed_sys(f) < v) __nanosleep(64);
+      SpinGuard g;  // a peer that never releases traps after kSpinLimitNs
+      while (ld_relaxed_sys(f) < v) {
+        __nanosleep(64);
+        g.tick();
+      }
     }
     fence_acq_rel_sys();
   } else {
     if (ld_relaxed(f) < v) {
-      while (ld_relaxed(f) < v) __nanosleep(32);
+      SpinGuard g;
+      while (ld_relaxed(f) < v) {
+        __nanosleep(32);
+        g.tick();
+      }
     }
     fence_acq_rel_gpu();
   }
@@ -979,7 +987,9 @@ __device__ __forceinline__ int bw_fetch(const double* xrows, int i, double* xi, 
     const double* src2 = xrows + (size_t)(also >= 0 ? also : i) * 3 * TS;
     unsigned long long v[6], w[6];
     bool ready, ready2;
+    SpinGuard g;
     do {
+      g.tick();
       ready = ready2 = true;
 #pragma unroll
       for (int e = 0; e < 6; ++e) {
@@ -1051,10 +1061,12 @@ __global__ void __launch_bounds__(256) k_dense_backward(DenseDev d, double* __re
       for (int i = j + tid; i <= N; i += 32) {
         const int* f = i == N ? d.flags + ntiles + j : d.flags + tidx(i, j);
         const int v = (i == j + 1 && i < N) ? 2 : 1;  // the sub-diagonal tile is final at 2
-        // bounded: a flag that never comes traps instead of hanging the device
-        for (long long spin = 0; ld_relaxed(f) < v; ++spin) {
-          if (spin > (1ll << 24)) __trap();
+        // bounded in time (SpinGuard): this CTA may wait for the whole
+        // factorization, so the bound is a clock limit, not a spin count
+        SpinGuard g;
+        while (ld_relaxed(f) < v) {
           __nanosleep(256);
+          g.tick();
         }
       }
       fence_acq_rel_gpu();

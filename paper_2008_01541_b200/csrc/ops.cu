@@ -10,6 +10,12 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+static int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
 namespace spb {
 void set_error(const std::string& msg);
 
@@ -392,7 +398,7 @@ int32_t spb_op_forward_sub(const spb_factor* fp, int64_t nrhs, const double* b1,
   }
   TMP(double, db, 3 * n);
   TMP(double, dy, 3 * std::max<int64_t>(n1, 1));
-  TMP(double, dU, 3 * (n1 > 0 ? std::max<size_t>(device_factor_ubuf(*f->dev), 1) : 1));
+  TMP(double, dU, 3 * (n1 > 0 ? std::max<size_t>(device_factor_ubuf(*f->dev_on(cur_device())), 1) : 1));
   TMP(double, df2, 3 * std::max<int64_t>(n2, 1));
   std::vector<double> bh(3 * n), yh(3 * n1), f2h(3 * n2);
   for (int64_t c0 = 0; c0 < nrhs; c0 += 3) {
@@ -403,7 +409,7 @@ int32_t spb_op_forward_sub(const spb_factor* fp, int64_t nrhs, const double* b1,
       for (int q = 0; q < 3 && c0 + q < nrhs; ++q) bh[3 * (n1 + k) + q] = b2[k * nrhs + c0 + q];
     H2D(db.p, bh.data(), sizeof(double) * 3 * n);
     if (n1 > 0) {
-      sparse_forward(0, *f->dev, db.p, dy.p, dU.p, df2.p, nullptr);
+      sparse_forward(0, *f->dev_on(cur_device()), db.p, dy.p, dU.p, df2.p, nullptr);
       SPB_CUDA(cudaGetLastError());
       D2H(yh.data(), dy.p, sizeof(double) * 3 * n1);
       if (n2 > 0) D2H(f2h.data(), df2.p, sizeof(double) * 3 * n2);
@@ -440,7 +446,7 @@ int32_t spb_op_backward_sub(const spb_factor* fp, int64_t nrhs, const double* y1
       for (int q = 0; q < 3 && c0 + q < nrhs; ++q) xf[3 * (n1 + k) + q] = x2[k * nrhs + c0 + q];
     H2D(dy.p, yh.data(), sizeof(double) * 3 * n1);
     H2D(dXF.p, xf.data(), sizeof(double) * 3 * n);
-    sparse_backward(0, *f->dev, dy.p, dXF.p, nullptr);
+    sparse_backward(0, *f->dev_on(cur_device()), dy.p, dXF.p, nullptr);
     SPB_CUDA(cudaGetLastError());
     D2H(xf.data(), dXF.p, sizeof(double) * 3 * n1);
     for (int64_t k = 0; k < n1; ++k)

@@ -843,8 +843,8 @@ constexpr int FL_ROWS = 32;
 
 __device__ __forceinline__ void flow_wait(const int* c, int need) {
   if (threadIdx.x == 0 && need > 0) {
-    while (ld_relaxed(c) < need) {
-    }
+    SpinGuard g;
+    while (ld_relaxed(c) < need) g.tick();
     fence_acq_rel_gpu();
   }
   __syncthreads();
@@ -1063,7 +1063,10 @@ static int upload(T** dst, const std::vector<T>& v) {
 }
 
 int build_device_factor(Factor& f) {
-  if (f.dev) return SPB_OK;
+  int cur = 0;
+  SPB_CUDA(cudaGetDevice(&cur));
+  if (cur < 0 || cur >= Factor::kMaxDevices) { set_error("device id out of range"); return SPB_ERR_ARG; }
+  if (f.devs[cur]) return SPB_OK;
   auto* d = new DeviceFactor();
   const int64_t ns = f.nsuper;
   d->n1 = (int)f.n1;
@@ -1418,7 +1421,7 @@ int build_device_factor(Factor& f) {
     d->fw_grid = std::max(1, nf) * NUM_SMS_B200;
     d->bw_grid = std::max(1, nb) * NUM_SMS_B200;
   }
-  f.dev = d;
+  f.devs[cur] = d;
   return SPB_OK;
 }
 
@@ -1519,4 +1522,13 @@ void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, do
 
 }  // namespace spb
 
-spb::Factor::~Factor() { delete dev; }
+spb::Factor::~Factor() {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  for (int k = 0; k < kMaxDevices; ++k)
+    if (devs[k]) {
+      cudaSetDevice(k);
+      delete devs[k];
+    }
+  if (cur >= 0) cudaSetDevice(cur);
+}

@@ -34,7 +34,11 @@ struct Factor {
   double maxdiag = 0.0;
   int64_t bad_column = -1;
   int64_t nnz_l1 = 0, nnz_c = 0;
-  DeviceFactor* dev = nullptr;     // lazily built, owned
+  // device copies, one per GPU (lazily built by build_device_factor on the
+  // current device, owned): contexts on different devices share one host factor
+  static constexpr int kMaxDevices = 16;
+  DeviceFactor* devs[kMaxDevices] = {};
+  DeviceFactor* dev_on(int device) const { return (device >= 0 && device < kMaxDevices) ? devs[device] : nullptr; }
 
   int build(int64_t n, int64_t n1, const int64_t* Ap, const int64_t* Ai, const double* Ax,
             const double* coords, int ordering, int relax);

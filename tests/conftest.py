@@ -27,3 +27,9 @@ def has_gpu() -> bool:
         return _native.device_count() > 0
     except Exception:
         return False
+
+
+# tests/ref_suite/ is the reference's own test suite, vendored verbatim: it
+# imports `schurpd` and runs only through tools/reference_suite.py (module
+# alias), from tests/test_gpu_reference_suite.py
+collect_ignore = ["ref_suite"]

@@ -1,7 +1,6 @@
-"""The REFERENCE's own test suite (138 tests of /root/reference/pkg/tests)
-run against this package through a `schurpd` module alias
-(tools/reference_suite.py). The copy lives in baseline/_ref/tests
-(git-ignored, like the rest of baseline/_ref); without it this test skips.
+"""The REFERENCE's own test suite (138 tests of /root/reference/pkg/tests,
+vendored verbatim in tests/ref_suite/) run against this package through a
+`schurpd` module alias (tools/reference_suite.py).
 
 Deselected, with the reason:
   * test_harness.py::test_cli_* (3): the reference CLI is out of scope;
@@ -9,7 +8,10 @@ Deselected, with the reason:
     ::test_early_exit_skips_remaining_outer_passes: they spy on the Python
     function collision.detect being called per pass; detection runs inside the
     device frame here. Their invariants (x1 frozen across inner passes, the
-    early exit) are checked on the device by tests/test_gpu_parity.py.
+    early exit) are checked on the device instead:
+    tests/test_gpu_parity.py::test_inner_keeps_x1_frozen_and_rhs_maintenance
+    and tests/test_gpu_early_exit.py (outer passes counted by the device,
+    states bitwise equal to the shortened frame).
 Everything else must pass (133 tests, incl. acceptance criteria 1-9)."""
 
 import subprocess
@@ -21,7 +23,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = Path(__file__).resolve().parent.parent
-SUITE = ROOT / "baseline" / "_ref" / "tests"
+SUITE = ROOT / "tests" / "ref_suite"
 
 DESELECT = [
     "test_harness.py::test_cli_run_and_errors",
@@ -32,8 +34,8 @@ DESELECT = [
 ]
 
 
-@pytest.mark.skipif(not SUITE.exists(), reason="baseline/_ref/tests not present (cp -r /root/reference/pkg/tests)")
 def test_reference_suite_passes():
+    assert (SUITE / "test_solver.py").exists(), "tests/ref_suite (vendored reference suite) is missing"
     args = [sys.executable, str(ROOT / "tools" / "reference_suite.py"), "-q", "-p", "no:randomly"]
     for d in DESELECT:
         args += ["--deselect", d]

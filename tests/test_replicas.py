@@ -79,7 +79,7 @@ def test_reference_arm_runs_on_rank0_only(monkeypatch, capsys):
     monkeypatch.setenv("WORLD_SIZE", "2")
 
     class Args:
-        config, outer, inner, steps, warmup, gpus, ref_frames = "cfg1", 1, 1, 2, 3, 2, 1
+        config, outer, inner, steps, warmup, gpus, ref_frames, collider = "cfg1", 1, 1, 2, 3, 2, 1, "plane"
 
     called = []
     monkeypatch.setattr(bench, "build_sim", lambda *a: called.append(a))
@@ -92,3 +92,31 @@ def test_single_process_max_is_identity():
 
     assert bench.max_over_ranks(None, 3.25) == 3.25
     assert bench.replica_throughput(1, 4.0) == 250.0
+
+
+def test_bench_spawns_one_rank_per_gpu():
+    """`python bench.py --gpus 2` (no WORLD_SIZE) re-launches itself under
+    torchrun with one process per GPU; each rank's scenes go to its own
+    device (LOCAL_RANK -> _native.default_device)."""
+    import json
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "SPB_DEVICE")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--probe-ranks"], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["world"] == 2
+    assert sorted(x["rank"] for x in line["ranks"]) == [0, 1]
+    assert sorted(x["device"] for x in line["ranks"]) == [0, 1]
+
+
+def test_spawn_command_layout():
+    import bench
+
+    cmd = bench.spawn_cmd(4, ["--gpus", "4", "--steps", "5"], 29555)
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd and "--master-port=29555" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "5"]

@@ -1,7 +1,7 @@
 """Run the REFERENCE's own test suite against this package:
 `schurpd` and its submodules are aliased to paper_2008_01541_b200, then
-pytest collects baseline/_ref/tests (a copy of /root/reference/pkg/tests,
-git-ignored like the rest of baseline/_ref, shipped to the GPU box).
+pytest collects tests/ref_suite (the reference's own tests, vendored
+verbatim from /root/reference/pkg/tests; see tests/ref_suite/README.md).
 
   python tools/reference_suite.py [pytest args]"""
 import importlib
@@ -32,7 +32,7 @@ sys.modules["schurpd.cli"] = _cli
 
 import pytest  # noqa: E402
 
-tests = ROOT / "baseline" / "_ref" / "tests"
-if not tests.exists():
-    sys.exit("baseline/_ref/tests missing: cp -r /root/reference/pkg/tests baseline/_ref/tests")
+tests = ROOT / "tests" / "ref_suite"
+if not (tests / "test_solver.py").exists():
+    sys.exit("tests/ref_suite missing (the vendored reference suite)")
 sys.exit(pytest.main([str(tests), "-p", "no:cacheprovider", "--rootdir", str(tests), *sys.argv[1:]]))
