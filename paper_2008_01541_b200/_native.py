@@ -214,7 +214,9 @@ def check(rc: int, column: Optional[int] = None) -> None:
 
 
 def ptr(a: Optional[np.ndarray]):
-    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+    """The buffer address as a plain int (every binding declares c_void_p,
+    which accepts it; cheaper per call than ctypes.data_as)."""
+    return None if a is None else a.ctypes.data
 
 
 def f64(a, shape=None) -> np.ndarray:

@@ -24,8 +24,17 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool owned = true;
+  // a non-owning view into a larger allocation (the packed small-IO block)
+  void view(T* ptr, size_t count) {
+    free();
+    p = ptr;
+    n = count;
+    owned = false;
+  }
   int alloc(size_t count) {
     free();
+    owned = true;
     n = count;
     if (cudaMalloc(&p, sizeof(T) * std::max<size_t>(count, 1)) != cudaSuccess) {
       p = nullptr;
@@ -48,7 +57,7 @@ struct DBuf {
     return SPB_OK;
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p && owned) cudaFree(p);
     p = nullptr;
     n = 0;
   }
@@ -138,6 +147,17 @@ struct Ctx {
   std::vector<double*> shape_vals;
   DBuf<ShapeDev> shapes_dev;
   bool shapes_dirty = true;
+  // Packed small-IO block: the per-frame inputs and outputs other than x
+  // live in ONE device allocation mirrored by ONE pinned host block, laid out
+  //   [colliders | attachment targets | active | target | f~2 | u2_accum | metrics | info]
+  // so spb_ctx_frame moves them with one H2D copy ([colliders .. target]) and
+  // one D2H copy ([active .. info]) instead of ~10 small transfers.
+  char* io_dev = nullptr;
+  char* io_small_host = nullptr;  // pinned
+  size_t io_small_bytes = 0;
+  size_t off_cols = 0, off_att = 0, off_act = 0, off_tgt = 0, off_f2 = 0, off_u2 = 0, off_met = 0, off_info = 0,
+         off_end = 0;
+  int setup_io_block();
   ColliderSet* cols_host = nullptr;  // pinned
   DBuf<ColliderSet> cols_dev;
   double* att_tgt_host = nullptr;    // pinned staging
@@ -147,6 +167,12 @@ struct Ctx {
   cudaStream_t st_aux = nullptr;     // sigma0 u2 + f~2 upkeep beside the backward sweep (last inner pass)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork0 = nullptr, ev_pre = nullptr;
   cudaEvent_t ph[6] = {};   // phase markers recorded inside the captured graphs (FrameMetrics phase times)
+  static constexpr int kMaxDetMarks = 8;
+  cudaEvent_t phd[2 * kMaxDetMarks] = {};  // detection start/end of the last outer pass's inner passes
+  int det_marks = 0;                       // detection pairs the last enqueue recorded
+  int last_det_marks = 0;                  // ... of the frame that ran last (graph or eager)
+  int last_ph_mask = 0;                    // which ph[] markers the last frame recorded
+  std::map<std::tuple<int, int, int>, int> graph_det_marks;
   bool last_graph = false;  // the last frame ran as a graph replay
   cudaEvent_t ev_state = nullptr;    // recorded between the solve and the metrics: the state is final
   // metrics
@@ -179,11 +205,10 @@ struct Ctx {
       cudaGraphExecDestroy(kv.second.second);
     }
     for (double* v : shape_vals) cudaFree(v);
-    if (cols_host) cudaFreeHost(cols_host);
-    if (att_tgt_host) cudaFreeHost(att_tgt_host);
+    if (io_small_host) cudaFreeHost(io_small_host);  // holds cols_host, att_tgt_host, metrics_host
+    if (io_dev) cudaFree(io_dev);
     if (io_host) cudaFreeHost(io_host);
     sweep_work_free(sw);
-    if (metrics_host) cudaFreeHost(metrics_host);
     if (pcg_host) cudaFreeHost(pcg_host);
     if (pcg_resid_host) cudaFreeHost(pcg_resid_host);
     if (eq_host) cudaFreeHost(eq_host);
@@ -195,6 +220,8 @@ struct Ctx {
     if (ev_fork0) cudaEventDestroy(ev_fork0);
     if (ev_pre) cudaEventDestroy(ev_pre);
     for (auto& e : ph)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : phd)
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
@@ -313,6 +340,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   SPB_CUDA(cudaEventCreateWithFlags(&ev_fork0, cudaEventDisableTiming));
   SPB_CUDA(cudaEventCreateWithFlags(&ev_pre, cudaEventDisableTiming));
   for (auto& e : ph) SPB_CUDA(cudaEventCreate(&e));
+  for (auto& e : phd) SPB_CUDA(cudaEventCreate(&e));
   SPB_CUDA(cudaEventCreateWithFlags(&ev_state, cudaEventDisableTiming));
   factor = f;
   n = s->num_nodes;
@@ -373,8 +401,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   std::vector<int> an(na);
   for (int a = 0; a < na; ++a) an[a] = (int)s->att_nodes[a];
   TRY(att_nodes.upload(an));
-  TRY(att_tgt.zeros(3 * (size_t)na));
-  SPB_CUDA(cudaMallocHost(&att_tgt_host, sizeof(double) * 3 * std::max(na, 1)));
+  TRY(setup_io_block());  // colliders, attachment targets, active, target, f~2, u2_accum, metrics, info
   TRY(b.zeros(3 * (size_t)n));
   TRY(y.zeros(3 * (size_t)std::max(n1, 1)));
   TRY(XF.zeros(3 * (size_t)n));
@@ -414,11 +441,7 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   pl_h = pl;
   TRY(prox_w.upload(s->proxy_weights, 4 * (size_t)P));
   TRY(prox_c.upload(s->proxy_stiffness, P));
-  TRY(active.zeros(std::max(P, 1)));
-  TRY(target.zeros(3 * (size_t)std::max(P, 1)));
   TRY(vprox.zeros(3 * (size_t)std::max(P, 1)));
-  TRY(f_tilde2.zeros(3 * (size_t)std::max(n2, 1)));
-  TRY(u2acc.zeros(3 * (size_t)std::max(n2, 1)));
   TRY(g.zeros(3 * (size_t)std::max(n2, 1)));
   TRY(u2.zeros(3 * (size_t)std::max(n2, 1)));
   TRY(s0u.zeros(3 * (size_t)std::max(n2, 1)));
@@ -456,7 +479,6 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
     TRY(Y.zeros((size_t)N * 4096));
     TRY(flags.zeros(nt + N));
     TRY(counter.zeros(1));
-    TRY(info.zeros(1));
     TRY(xrows.zeros((size_t)N * 3 * 64));
     TRY(gemv_partial.zeros((size_t)nt * 6 * 64));
     std::vector<int2> tk = cholesky_task_order(N, true, CHOL_LEAD);
@@ -497,9 +519,6 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
                   c22_tile_ptr.p, c22_ent_rc.p, c22_ent_ptr.p, c22_contrib.p, prox_w.p, prox_c.p, active.p};
   }
   // colliders + metrics
-  SPB_CUDA(cudaMallocHost(&cols_host, sizeof(ColliderSet)));
-  memset(cols_host, 0, sizeof(ColliderSet));
-  TRY(cols_dev.zeros(1));
   e_blocks = energy_blocks(ne);
   a_blocks = attachment_blocks(na);
   p_blocks = proxy_blocks(P);
@@ -508,9 +527,38 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
   TRY(a_part.zeros(std::max(a_blocks, 1)));
   TRY(p_part.zeros(2 * (size_t)std::max(p_blocks, 1)));
   TRY(r_part.zeros(2 * (size_t)std::max(r_blocks, 1)));
-  TRY(metrics_out.zeros(4));
-  SPB_CUDA(cudaMallocHost(&metrics_host, sizeof(double) * 5));  // 4 metrics + the info word
   SPB_CUDA(cudaDeviceSynchronize());
+  return SPB_OK;
+}
+
+int Ctx::setup_io_block() {
+  auto up = [](size_t v) { return (v + 255) & ~size_t(255); };
+  size_t o = 0;
+  off_cols = o; o = up(o + sizeof(ColliderSet));
+  off_att = o;  o = up(o + sizeof(double) * 3 * std::max(na, 1));
+  off_act = o;  o = up(o + (size_t)std::max(P, 1));
+  off_tgt = o;  o = up(o + sizeof(double) * 3 * std::max(P, 1));
+  off_f2 = o;   o = up(o + sizeof(double) * 3 * std::max(n2, 1));
+  off_u2 = o;   o = up(o + sizeof(double) * 3 * std::max(n2, 1));
+  off_met = o;  o += sizeof(double) * 4;  // metrics_host[4] is the info word (as before)
+  off_info = o; o = up(o + sizeof(int));
+  off_end = o;
+  io_small_bytes = o;
+  SPB_CUDA(cudaMalloc(&io_dev, io_small_bytes));
+  SPB_CUDA(cudaMemset(io_dev, 0, io_small_bytes));
+  SPB_CUDA(cudaMallocHost(&io_small_host, io_small_bytes));
+  memset(io_small_host, 0, io_small_bytes);
+  cols_dev.view(reinterpret_cast<ColliderSet*>(io_dev + off_cols), 1);
+  att_tgt.view(reinterpret_cast<double*>(io_dev + off_att), 3 * (size_t)na);
+  active.view(reinterpret_cast<uint8_t*>(io_dev + off_act), (size_t)std::max(P, 1));
+  target.view(reinterpret_cast<double*>(io_dev + off_tgt), 3 * (size_t)std::max(P, 1));
+  f_tilde2.view(reinterpret_cast<double*>(io_dev + off_f2), 3 * (size_t)std::max(n2, 1));
+  u2acc.view(reinterpret_cast<double*>(io_dev + off_u2), 3 * (size_t)std::max(n2, 1));
+  metrics_out.view(reinterpret_cast<double*>(io_dev + off_met), 4);
+  info.view(reinterpret_cast<int*>(io_dev + off_info), 1);
+  cols_host = reinterpret_cast<ColliderSet*>(io_small_host + off_cols);
+  att_tgt_host = reinterpret_cast<double*>(io_small_host + off_att);
+  metrics_host = reinterpret_cast<double*>(io_small_host + off_met);  // [4 metrics][info word]
   return SPB_OK;
 }
 
@@ -555,7 +603,7 @@ void Ctx::drop_graphs() {
 // acceptance test 7 measures). use_graph=False times every phase.
 // SPB_PHASE_MARKERS=63 records all six (diagnostics).
 static int graph_marker_mask() {
-  static const int m = getenv("SPB_PHASE_MARKERS") ? atoi(getenv("SPB_PHASE_MARKERS")) : 12;
+  static const int m = getenv("SPB_PHASE_MARKERS") ? atoi(getenv("SPB_PHASE_MARKERS")) : 31;
   return m;
 }
 static cudaError_t mark_phase(cudaEvent_t* ev, int k, cudaStream_t st) {
@@ -571,6 +619,17 @@ static bool marker_on(int k) {
   return (graph_marker_mask() >> k) & 1;
 }
 
+// detection span markers (FrameMetrics.t_detect_ms): always recorded, as
+// external event nodes under capture (off the PDL chains: the first pass's
+// detection runs on the aux stream)
+static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(st, &cs);
+  if (err != cudaSuccess) return err;
+  if (cs != cudaStreamCaptureStatusActive) return cudaEventRecord(e, st);
+  return cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+}
+
 int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
   struct PdlScope {  // concurrent scenes (aux_overlap off): no programmatic launches
     bool prev;
@@ -582,6 +641,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
   bool first_detection_done = false;
   bool aux_pending = false;
   residual_valid = false;
+  det_marks = 0;
   if (ev) SPB_CUDA(mark_phase(ev, 0, st));
   static const bool aux_on = !(getenv("SPB_AUX_OVERLAP") && getenv("SPB_AUX_OVERLAP")[0] == '0');
   for (int o = 0; o < outer; ++o) {
@@ -594,7 +654,10 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       SPB_CUDA(cudaStreamWaitEvent(st_aux, ev_fork0, 0));
       const bool fresh0 = cadence == SPB_CADENCE_INNER || (cadence == SPB_CADENCE_FRAME && !first_detection_done);
       if (fresh0 && P > 0) {
+        const bool mk = ev && o == outer - 1 && det_marks < kMaxDetMarks;
+        if (mk) SPB_CUDA(mark_event(phd[2 * det_marks], st_aux));
         launch_detect(st_aux, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
+        if (mk) SPB_CUDA(mark_event(phd[2 * det_marks++ + 1], st_aux));
         launches++;
       }
       launch_local_forces(st_aux, nbeta, e_beta.p, tets.p, x.p, dmi.p, vol.p, ne, R.p, Q.p, ep, Gb.p, 1);
@@ -627,7 +690,10 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
         first_detection_done = true;
       } else {
         if (fresh && P > 0) {
+          const bool mk = ev && o == outer - 1 && det_marks < kMaxDetMarks;
+          if (mk) SPB_CUDA(mark_event(phd[2 * det_marks], st));
           launch_detect(st, P_, tets.p, x.p, shapes_dev.p, cols_dev.p, active.p, target.p, nullptr);
+          if (mk) SPB_CUDA(mark_event(phd[2 * det_marks++ + 1], st));
           launches++;
         }
         first_detection_done = true;
@@ -1094,10 +1160,12 @@ static int ensure_graphs(Ctx* c, const spb_step_config* cfg,
   if (it == c->graphs.end()) {
     {
       cudaGraphExec_t exe[2];
+      int det = 0;
       for (int part = 0; part < 2; ++part) {
         cudaGraph_t gph;
         SPB_CUDA(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
         int rc = part == 0 ? c->enqueue_solve(outer, inner, cad, c->ph) : c->enqueue_metrics(c->ph);
+        if (part == 0) det = c->det_marks;
         cudaError_t e2 = cudaStreamEndCapture(c->st, &gph);
         if (rc != SPB_OK) return rc;
         if (e2 != cudaSuccess) { spb::set_error(std::string("graph capture: ") + cudaGetErrorString(e2)); return SPB_ERR_CUDA; }
@@ -1105,6 +1173,7 @@ static int ensure_graphs(Ctx* c, const spb_step_config* cfg,
         SPB_CUDA(cudaGraphUpload(exe[part], c->st));  // the first launch pays no upload
         cudaGraphDestroy(gph);
       }
+      c->graph_det_marks[key] = det;
       it = c->graphs.emplace(key, std::make_pair(exe[0], exe[1])).first;
     }
   }
@@ -1120,11 +1189,18 @@ static int ensure_graphs(Ctx* c, const spb_step_config* cfg,
 static int run_frame_early_exit(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
   TRY(c->ensure_pose_gather());
   c->last_graph = false;
+  if (!ev) {
+    ev = c->ph;
+    c->last_ph_mask = 63;
+  } else {
+    c->last_ph_mask = 0;
+  }
   int launches = 0;
   c->outer_passes = 0;
   for (int o = 0; o < cfg->outer_iters; ++o) {
     const int cad = (o > 0 && cfg->cadence == SPB_CADENCE_FRAME) ? SPB_CADENCE_NEVER : cfg->cadence;
     TRY(c->enqueue_solve(1, cfg->inner_iters, cad, ev));
+    c->last_det_marks = c->det_marks;
     TRY(c->enqueue_equilibrium_residual());
     launches += c->last_launches;
     SPB_CUDA(cudaStreamSynchronize(c->st));
@@ -1146,22 +1222,35 @@ static int run_frame(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
     std::map<std::tuple<int, int, int>, std::pair<cudaGraphExec_t, cudaGraphExec_t>>::iterator it;
     TRY(ensure_graphs(c, cfg, &it));
     c->last_graph = true;
+    c->last_det_marks = c->graph_det_marks[it->first];
+    c->last_ph_mask = spb::graph_marker_mask();
     SPB_CUDA(cudaGraphLaunch(it->second.first, c->st));
     SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
     SPB_CUDA(cudaGraphLaunch(it->second.second, c->st));
     return SPB_OK;
   }
   c->last_graph = false;
+  // an eager frame records every phase marker (plain event records)
+  if (!ev) {
+    ev = c->ph;
+    c->last_ph_mask = 63;
+  } else {
+    c->last_ph_mask = 0;  // the caller's own events (spb_ctx_step)
+  }
   TRY(c->enqueue_solve(outer, inner, cad, ev));
+  c->last_det_marks = c->det_marks;
   SPB_CUDA(cudaEventRecord(c->ev_state, c->st));
   return c->enqueue_metrics(ev);
 }
 
 // Enqueue one frame and the metrics read-back; no synchronisation.
-static int frame_enqueue(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
+// packed: the caller downloads the whole [active .. info] region itself (one
+// copy, spb_ctx_frame); otherwise the metrics and the info word come back here.
+static int frame_enqueue(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev, bool packed = false) {
   if (cfg->outer_iters < 1 || cfg->inner_iters < 1) { spb::set_error("outer_iters and inner_iters must be >= 1"); return SPB_ERR_ARG; }
   if (c->n2 > 0) SPB_CUDA(cudaMemsetAsync(c->info.p, 0, sizeof(int), c->st));
   TRY(run_frame(c, cfg, ev));
+  if (packed) return SPB_OK;
   SPB_CUDA(cudaMemcpyAsync(c->metrics_host, c->metrics_out.p, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->st));
   int* info_h = reinterpret_cast<int*>(c->metrics_host + 4);
   *info_h = 0;
@@ -1171,13 +1260,22 @@ static int frame_enqueue(Ctx* c, const spb_step_config* cfg, cudaEvent_t* ev) {
 
 // After the stream has drained: metrics out, SPB_ERR_INDEFINITE on a bad pivot.
 static int frame_finish(Ctx* c, spb_frame_metrics* m) {
-  if (c->last_graph && m->t_local_ms == 0.0) {
-    // phase split from the markers inside the replayed graphs (the last pass)
+  if (c->last_ph_mask && m->t_local_ms == 0.0) {
+    // phase split from the markers of the last outer pass (inside the
+    // replayed graphs, or recorded by an eager frame)
     float a = 0.f;
     double* out[4] = {&m->t_local_ms, &m->t_forward_ms, &m->t_dense_ms, &m->t_backward_ms};
     for (int k = 0; k < 4; ++k)
-      if (spb::marker_on(k) && spb::marker_on(k + 1) && cudaEventElapsedTime(&a, c->ph[k], c->ph[k + 1]) == cudaSuccess)
+      if (((c->last_ph_mask >> k) & 3) == 3 && cudaEventElapsedTime(&a, c->ph[k], c->ph[k + 1]) == cudaSuccess)
         *out[k] = a;
+    cudaGetLastError();
+  }
+  if (m->t_detect_ms == 0.0) {
+    // detection kernels of the last outer pass (device time between the
+    // marker pair around each launch)
+    float a = 0.f;
+    for (int k = 0; k < c->last_det_marks; ++k)
+      if (cudaEventElapsedTime(&a, c->phd[2 * k], c->phd[2 * k + 1]) == cudaSuccess) m->t_detect_ms += a;
     cudaGetLastError();
   }
   m->energy = c->metrics_host[0];
@@ -1228,24 +1326,81 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
   SPB_CUDA(cudaSetDevice(c->device));
   auto t0 = std::chrono::steady_clock::now();
   memset(m, 0, sizeof(*m));
+  if (ncol > spb::MAX_COLLIDERS) { spb::set_error("too many colliders"); return SPB_ERR_ARG; }
   SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
-  TRY(pose_upload(c, att_targets, ncol, cols));
+  // SPB_IO_TRACE=1: device-side spans of the call (upload, frame, download)
+  static const bool io_trace = getenv("SPB_IO_TRACE") && getenv("SPB_IO_TRACE")[0] == '1';
+  cudaEvent_t tev[4] = {};
+  auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+  double th[4] = {};
+  if (io_trace) {
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], c->st);
+    th[0] = host_ms();
+  }
+  // ---- inputs: x by DMA (page-locked by the caller) or staged; everything
+  // else (pose, active, target) packed into the pinned small-IO block and
+  // moved by ONE copy
+  char* hs = c->io_small_host;
+  if (c->na > 0 && att_targets) memcpy(hs + c->off_att, att_targets, sizeof(double) * 3 * c->na);
+  c->cols_host->n = ncol;
+  for (int i = 0; i < ncol; ++i) {
+    if (cols[i].shape < 0 || cols[i].shape >= (int)c->shapes.size()) {
+      spb::set_error("unknown collider shape id");
+      return SPB_ERR_ARG;
+    }
+    c->cols_host->posed[i].shape = cols[i].shape;
+    memcpy(c->cols_host->posed[i].R, cols[i].rotation, sizeof(double) * 9);
+    memcpy(c->cols_host->posed[i].t, cols[i].translation, sizeof(double) * 3);
+  }
+  if (c->P) {
+    memcpy(hs + c->off_act, active, c->P);
+    memcpy(hs + c->off_tgt, target, sizeof(double) * 3 * c->P);
+  }
+  TRY(c->sync_shapes());
+  const size_t up_bytes = c->P ? c->off_tgt + sizeof(double) * 3 * c->P : c->off_act;
+  SPB_CUDA(cudaMemcpyAsync(c->io_dev, hs, up_bytes, cudaMemcpyHostToDevice, c->st));
   IoList up;
   up.add(c->x.p, x, sizeof(double) * 3 * c->n);
-  if (c->P) up.add(c->active.p, active, c->P);
-  if (c->P) up.add(c->target.p, target, sizeof(double) * 3 * c->P);
   TRY(io_upload(c, up, false));
-  TRY(frame_enqueue(c, cfg, nullptr));
+  if (io_trace) {
+    cudaEventRecord(tev[1], c->st);
+    th[1] = host_ms();
+  }
+  TRY(frame_enqueue(c, cfg, nullptr, true));
+  if (io_trace) {
+    cudaEventRecord(tev[2], c->st);
+    th[2] = host_ms();
+  }
+  // ---- outputs: x on the io stream from the in-graph "state final" event,
+  // overlapping the metrics kernels; [active .. info] (active, target, f~2,
+  // u2_accum, metrics, info) in one copy behind the metrics
+  SPB_CUDA(cudaMemcpyAsync(hs + c->off_act, c->io_dev + c->off_act, c->off_end - c->off_act,
+                           cudaMemcpyDeviceToHost, c->st));
   IoList down;
   down.add(c->x.p, x, sizeof(double) * 3 * c->n);
-  if (c->P) down.add(c->active.p, active, c->P);
-  if (c->P) down.add(c->target.p, target, sizeof(double) * 3 * c->P);
-  if (c->n2) down.add(c->f_tilde2.p, f_tilde2, sizeof(double) * 3 * c->n2);
-  if (c->n2) down.add(c->u2acc.p, u2_accum, sizeof(double) * 3 * c->n2);
-  // the download runs on the io stream from the in-graph "state final" event
-  // (behind the upload's copies, which precede the graph on the main stream),
-  // overlapping the metrics kernels; both streams are synchronised
-  TRY(io_download(c, down, c->st_io, true));
+  TRY(io_download(c, down, c->st_io, true));  // synchronises both streams
+  if (c->P) {
+    memcpy(active, hs + c->off_act, c->P);
+    memcpy(target, hs + c->off_tgt, sizeof(double) * 3 * c->P);
+  }
+  if (c->n2) {
+    if (f_tilde2) memcpy(f_tilde2, hs + c->off_f2, sizeof(double) * 3 * c->n2);
+    if (u2_accum) memcpy(u2_accum, hs + c->off_u2, sizeof(double) * 3 * c->n2);
+  }
+  if (c->n2 == 0) *reinterpret_cast<int*>(c->metrics_host + 4) = 0;
+  if (io_trace) {
+    th[3] = host_ms();
+    cudaEventRecord(tev[3], c->st_io);
+    cudaEventSynchronize(tev[3]);
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&b, tev[1], tev[2]);
+    cudaEventElapsedTime(&d, tev[2], tev[3]);
+    fprintf(stderr, "[io] gpu: upload %.3f frame %.3f download %.3f ms | host: enter->upload-issued %.3f "
+            "->frame-issued %.3f ->synced %.3f ms\n", a, b, d, th[1], th[2], th[3]);
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return frame_finish(c, m);
   SPB_GUARD_END

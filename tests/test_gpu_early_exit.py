@@ -67,17 +67,20 @@ def test_early_exit_per_pass_path_equals_fused_frame(cadence):
 
 
 def test_early_exit_threshold_matches_reference_residual():
-    """The device RMS is the reference's _equilibrium_residual: a threshold
-    just above the host-evaluated residual after pass 1 stops after pass 1;
-    one just below it does not."""
+    """The device RMS is the reference's _equilibrium_residual. After a pass
+    the forces are evaluated with the rotations that pass solved with, so the
+    residual is at roundoff level (~1e-13 here) and its last digits depend on
+    summation order: a threshold 1e3x above the host-evaluated value stops
+    after pass 1, one 1e3x below it does not."""
     model, system, state, _ = make_bar(press_depth=0.08)
     s1 = state.copy()
     _passes(model, system, s1, 1, 1)
     r1 = sol._equilibrium_residual(model, s1)  # host restatement of solver.py:468-471 (test-side check)
+    assert 0.0 < r1 < 1e-6
     st = state.copy()
-    assert _passes(model, system, st, 4, 1, early=r1 * (1 + 1e-9)) == 1
+    assert _passes(model, system, st, 4, 1, early=r1 * 1e3) == 1
     st = state.copy()
-    assert _passes(model, system, st, 4, 1, early=r1 * (1 - 1e-9)) > 1
+    assert _passes(model, system, st, 4, 1, early=r1 * 1e-3) > 1
 
 
 def test_early_exit_pcg():

@@ -301,3 +301,20 @@ def test_sweep_variants_match(monkeypatch, env):
     alt = sweep(env)
     for a, b in zip(ref, alt):
         assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_frame_metrics_phase_split(graph):
+    """FrameMetrics carries the reference's phase split every frame
+    (solver.py:402-446: t_local, t_forward, t_detect, t_dense, t_backward),
+    on the graph-replay path as well as eagerly: device times from event
+    markers of the last outer pass (detection: around each launch)."""
+    model, system, state, _ = make_bar(press_depth=0.08)
+    cfg = sol.SolverConfig(outer_iters=1, inner_iters=2, use_graph=graph)
+    for _ in range(3):
+        met = sol.solve_frame_schur(model, system, state, cfg)
+    for k in ("t_local_ms", "t_forward_ms", "t_detect_ms", "t_dense_ms", "t_backward_ms"):
+        assert getattr(met, k) > 0.0, k
+    parts = met.t_local_ms + met.t_forward_ms + met.t_dense_ms + met.t_backward_ms
+    assert parts <= met.t_total_ms
+    assert met.t_detect_ms <= met.t_total_ms
