@@ -214,8 +214,13 @@ def check(rc: int, column: Optional[int] = None) -> None:
 
 
 def ptr(a: Optional[np.ndarray]):
-    """The buffer address as a plain int (every binding declares c_void_p,
-    which accepts it; cheaper per call than ctypes.data_as)."""
+    """A c_void_p that also keeps `a` alive (call sites pass temporaries)."""
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def addr(a: Optional[np.ndarray]):
+    """The bare buffer address (int) for the per-frame hot path: cheaper than
+    ptr(), but the CALLER must hold a reference to `a` for the call."""
     return None if a is None else a.ctypes.data
 
 

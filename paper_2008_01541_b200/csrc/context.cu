@@ -730,8 +730,15 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
         su = st_aux;
         launches++;
       }
-      launch_sym_tile_gemv(su, dd, u2.p, gemv_partial.p);
-      launch_sym_tile_gemv_reduce(su, dd, gemv_partial.p, s0u.p);
+      // on the main stream the streaming (persistent, TMA-fed) mat-vec; beside
+      // the backward sweep the short-lived per-tile kernel, whose CTAs hold no
+      // shared memory and so leave the sweep's level kernels their SM slots
+      if (overlap) {
+        launch_sym_tile_gemv(su, dd, u2.p, gemv_partial.p);
+        launch_sym_tile_gemv_reduce(su, dd, gemv_partial.p, s0u.p);
+      } else {
+        launch_sym_gemv(su, dd, u2.p, gemv_partial.p, s0u.p, true);
+      }
       launch_proxy_wu(su, P_, active.p, u2.p, vprox.p);
       launch_inner_update(su, n2, u2.p, s0u.p, k_ptr.p, k_idx.p, k_val.p, g.p, prox_w.p, vprox.p, gc_ptr.p,
                           gc_src.p, f_tilde2.p, overlap ? nullptr : u2acc.p, x.p, x2_ids.p, r_part.p);
@@ -1607,8 +1614,7 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
       break;
     case 1: spb::launch_dense_backward(c->st, c->dd, c->xrows.p, c->u2.p); break;
     case 2:
-      spb::launch_sym_tile_gemv(c->st, c->dd, c->u2.p, c->gemv_partial.p);
-      spb::launch_sym_tile_gemv_reduce(c->st, c->dd, c->gemv_partial.p, c->s0u.p);
+      spb::launch_sym_gemv(c->st, c->dd, c->u2.p, c->gemv_partial.p, c->s0u.p, true);
       break;
     case 3: spb::sparse_forward(c->st, *c->factor->dev_on(c->device), c->b.p, c->y.p, c->U.p, c->f_tilde2.p, nullptr, &c->sw); break;
     case 4: spb::sparse_backward(c->st, *c->factor->dev_on(c->device), c->y.p, c->XF.p, nullptr, &c->sw); break;

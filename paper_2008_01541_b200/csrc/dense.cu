@@ -1256,6 +1256,204 @@ __global__ void __launch_bounds__(256) k_sym_gemv_tiles(DenseDev d, const double
   }
 }
 
+// ---------------------------------------------- streaming symmetric mat-vec
+// partial = per-tile products of sigma0 u (3 RHS) over the lower tiles
+// (solver.py:436-440: the f~2 upkeep and the residual share this one pass).
+// Persistent: every CTA streams tiles t = blockIdx.x + k * gridDim.x through a
+// 3-stage ring of 32 KB bulk copies (cp.async.bulk + mbarrier), so HBM sees a
+// continuous stream instead of one short-lived CTA per tile; the u blocks of
+// the next tile are prefetched into registers while the current one computes.
+//   row part    (block row i): T u_j on the FP64 tensor pipe (DMMA m8n8k4,
+//               RHS in the n dimension): warp w owns rows 8w..8w+7, 16 k-steps;
+//               the fragments read the swizzled tile conflict-free;
+//   column part (block j, i != j): T^T u_i with FMAs, thread = column,
+//               16 rows per thread, 4 row groups summed in fixed order.
+// k_sym_gemv_reduce4 then sums every block's partials in fixed tile order.
+#ifndef SG_STAGES_CFG
+#define SG_STAGES_CFG 2
+#define SG_CTAS_CFG 3
+#endif
+constexpr int SG_STAGES = SG_STAGES_CFG;
+constexpr int SG_THREADS = 256;
+constexpr int SG_CTAS_PER_SM = SG_CTAS_CFG;
+constexpr size_t SG_SMEM = (size_t)SG_STAGES * TILE_BYTES + 8 * (6 * TS + 4 * 3 * TS + 3 * TS) + 64;
+
+__device__ __forceinline__ void sgemv_tile_ij(int t, int& i, int& j) {
+  i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while (tidx(i + 1, 0) <= t) ++i;
+  while (tidx(i, 0) > t) --i;
+  j = t - tidx(i, 0);
+}
+
+__global__ void __launch_bounds__(SG_THREADS, SG_CTAS_PER_SM) k_sym_gemv_stream(
+    DenseDev d, const double* __restrict__ u, double* __restrict__ partial) {
+  extern __shared__ __align__(128) double sgm[];
+  double* stage = sgm;                      // SG_STAGES x 64 x 64 (swizzled, as in global)
+  double* ubuf = sgm + SG_STAGES * TILE;    // [u_i (3 x 64) | u_j (3 x 64)], RHS-major
+  double* colred = ubuf + 6 * TS;           // 4 row groups x 3 x 64
+  double* rowout = colred + 4 * 3 * TS;     // 3 x 64
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(rowout + 3 * TS);  // SG_STAGES
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int ntiles = d.N * (d.N + 1) / 2;
+  const int m = d.m;
+  if (tid == 0) {
+    for (int k = 0; k < SG_STAGES; ++k) mbar_init(&full[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int nmine = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) ++nmine;
+  if (tid == 0) {  // sigma0 is constant: the ring fills while the predecessor finishes
+    for (int k = 0; k < SG_STAGES && k < nmine; ++k) {
+      const int t = blockIdx.x + k * gridDim.x;
+      mbar_expect_tx(&full[k], TILE_BYTES);
+      bulk_g2s(stage + k * TILE, d.sigma0 + (size_t)t * TILE, TILE_BYTES, &full[k]);
+    }
+  }
+  pdl_wait();  // u comes from the predecessor (dense backward solve)
+  double pu[6];
+  {
+    int i, j;
+    sgemv_tile_ij(blockIdx.x, i, j);
+    if (tid < TS && nmine > 0) {
+      const int ri = i * TS + tid, rj = j * TS + tid;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        pu[q] = ri < m ? u[3 * ri + q] : 0.0;
+        pu[3 + q] = rj < m ? u[3 * rj + q] : 0.0;
+      }
+    }
+  }
+  for (int k = 0; k < nmine; ++k) {
+    const int t = blockIdx.x + k * gridDim.x;
+    const int sidx = k % SG_STAGES;
+    double* ui = ubuf;  // rewritten only after the previous tile's last barrier
+    double* uj = ui + 3 * TS;
+    int i, j;
+    sgemv_tile_ij(t, i, j);
+    if (tid < TS) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        ui[q * TS + tid] = pu[q];
+        uj[q * TS + tid] = pu[3 + q];
+      }
+      // prefetch the next tile's u blocks (latency hidden behind this tile)
+      if (k + 1 < nmine) {
+        int i2, j2;
+        sgemv_tile_ij(t + gridDim.x, i2, j2);
+        const int ri = i2 * TS + tid, rj = j2 * TS + tid;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          pu[q] = ri < m ? u[3 * ri + q] : 0.0;
+          pu[3 + q] = rj < m ? u[3 * rj + q] : 0.0;
+        }
+      }
+    }
+    __syncthreads();  // u blocks staged; the previous tile's rowout/colred were read
+    mbar_wait(&full[sidx], (k / SG_STAGES) & 1);
+    const double* T = stage + sidx * TILE;
+    // ---- row part on DMMA: rows 8w + g8, RHS in n (columns 0..2 of 8);
+    // two accumulator chains (even / odd k-steps) summed at the end
+    {
+      // four independent accumulator chains (k-steps mod 4), summed in fixed order
+      double cc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const int r = 8 * warp + g8;
+#pragma unroll
+      for (int ks = 0; ks < 16; ks += 4) {
+        double a[4], bb[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          a[h] = T[swz(r, 4 * (ks + h) + t4)];
+          bb[h] = g8 < 3 ? uj[g8 * TS + 4 * (ks + h) + t4] : 0.0;
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) dmma(cc[h][0], cc[h][1], a[h], bb[h]);
+      }
+      const double c0 = (cc[0][0] + cc[1][0]) + (cc[2][0] + cc[3][0]);
+      const double c1 = (cc[0][1] + cc[1][1]) + (cc[2][1] + cc[3][1]);
+      // lane (g8, t4) holds C[g8][2 t4], C[g8][2 t4 + 1]: RHS 0,1 (t4 = 0), RHS 2 (t4 = 1)
+      if (t4 == 0) {
+        rowout[0 * TS + r] = c0;
+        rowout[1 * TS + r] = c1;
+      } else if (t4 == 1) {
+        rowout[2 * TS + r] = c0;
+      }
+    }
+    // ---- column part: thread = column c, rows 16 g .. 16 g + 15
+    if (i != j) {
+      const int c = tid & 63, g = tid >> 6;
+      double sv[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // even / odd rows
+#pragma unroll
+      for (int rr = 0; rr < 16; ++rr) {
+        const int r = 16 * g + rr;
+        const double a = T[swz(r, c)];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) sv[rr & 1][q] = fma(a, ui[q * TS + r], sv[rr & 1][q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) colred[(g * 3 + q) * TS + c] = sv[0][q] + sv[1][q];
+    }
+    __syncthreads();  // stage sidx is free; rowout/colred complete
+    if (tid == 0 && k + SG_STAGES < nmine) {
+      const int tn = blockIdx.x + (k + SG_STAGES) * gridDim.x;
+      fence_proxy_async_smem();
+      mbar_expect_tx(&full[sidx], TILE_BYTES);
+      bulk_g2s(stage + sidx * TILE, d.sigma0 + (size_t)tn * TILE, TILE_BYTES, &full[sidx]);
+    }
+    double* out_row = partial + (size_t)t * 6 * TS;
+    double* out_col = out_row + 3 * TS;
+    if (tid < 3 * TS) {
+      out_row[tid] = rowout[tid];
+      if (i != j) {
+        const int q = tid / TS, c = tid % TS;
+        out_col[tid] = ((colred[(0 * 3 + q) * TS + c] + colred[(1 * 3 + q) * TS + c]) +
+                        colred[(2 * 3 + q) * TS + c]) + colred[(3 * 3 + q) * TS + c];
+      }
+    }
+  }
+  if (tid == 0) pdl_trigger();
+}
+
+// out[b] = the sum over the tiles of block row/column b in fixed tile order:
+// 4 thread groups each sum a fixed quarter of the tiles, then group 0 adds
+// the four quarter sums in fixed order (4x the loads in flight of a single
+// sequential sum; bitwise deterministic).
+__global__ void __launch_bounds__(768) k_sym_gemv_reduce4(DenseDev d, const double* __restrict__ partial,
+                                                          double* __restrict__ out) {
+  __shared__ double qs[4][3 * TS];
+  pdl_wait();
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int grp = tid / (3 * TS), e = tid % (3 * TS);
+  const int q = e / TS, r = e % TS;
+  const int N = d.N;  // block b touches N tiles: (b, 0..b) then (b+1..N-1, b)
+  const int k0 = (grp * N) / 4, k1 = ((grp + 1) * N) / 4;
+  double s = 0.0;
+  int k = k0;
+  for (; k + 8 <= k1; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const int kk = k + h;
+      v[h] = kk <= b ? partial[(size_t)tidx(b, kk) * 6 * TS + q * TS + r]
+                     : partial[(size_t)tidx(kk, b) * 6 * TS + 3 * TS + q * TS + r];
+    }
+#pragma unroll
+    for (int h = 0; h < 8; ++h) s += v[h];
+  }
+  for (; k < k1; ++k)
+    s += k <= b ? partial[(size_t)tidx(b, k) * 6 * TS + q * TS + r]
+                : partial[(size_t)tidx(k, b) * 6 * TS + 3 * TS + q * TS + r];
+  qs[grp][e] = s;
+  __syncthreads();
+  if (grp == 0) {
+    const double tot = ((qs[0][e] + qs[1][e]) + qs[2][e]) + qs[3][e];
+    const int row = b * TS + r;
+    if (row < d.m) out[3 * row + q] = tot;
+  }
+  if (tid == 0) pdl_trigger();
+}
+
 // out[b] = sum over the tiles of block row/column b, in fixed order (loads
 // unrolled so they are in flight together; the adds stay sequential)
 __global__ void k_sym_gemv_reduce(DenseDev d, const double* __restrict__ partial, double* __restrict__ out) {
@@ -1338,6 +1536,29 @@ void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, d
 
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out) {
   k_sym_gemv_reduce<<<d.N, 192, 0, st>>>(d, partial, out);
+}
+
+// out = sigma0 u: the streaming tile pass, then the fixed-order block sums
+// (both programmatic launches when pdl).
+void launch_sym_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial, double* out, bool pdl) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sym_gemv_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG_SMEM);
+    attr = true;
+  }
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sym_gemv_stream, SG_THREADS, SG_SMEM);
+    per_sm = std::max(1, std::min(per_sm, SG_CTAS_PER_SM));
+  }
+  const int grid = std::min(dense_tile_count(d.N), NUM_SMS_B200 * per_sm);
+  if (pdl) {
+    launch_pdl(k_sym_gemv_stream, dim3(grid), dim3(SG_THREADS), SG_SMEM, st, d, u, partial);
+    launch_pdl(k_sym_gemv_reduce4, dim3(d.N), dim3(4 * 3 * TS), 0, st, d, (const double*)partial, out);
+    return;
+  }
+  k_sym_gemv_stream<<<grid, SG_THREADS, SG_SMEM, st>>>(d, u, partial);
+  k_sym_gemv_reduce4<<<d.N, 4 * 3 * TS, 0, st>>>(d, partial, out);
 }
 
 // Task order: column-major (below-diagonal tiles, RHS row), with diagonal
