@@ -138,6 +138,9 @@ struct Ctx {
   bool aux_overlap = true;  // second-stream overlap of the last inner pass (off for concurrent scenes)
   DBuf<double> sigma0_tiles, L, LinvT, Y, gemv_partial, xrows;
   DBuf<int> flags, counter, info;
+  bool oz = false;           // factorization with the k-loop on the INT8 tensor cores (k_cholesky_oz)
+  DBuf<int> erow;            // per-row exponent bounds (INT8 path)
+  DBuf<signed char> Lq;      // digit planes of the L tiles (INT8 path)
   SweepWork sw;  // sparse-sweep workspace of this context
   DBuf<int2> tasks;
   DBuf<int> c22_tile_ptr, c22_ent_rc, c22_ent_ptr, c22_contrib;
@@ -517,6 +520,31 @@ int Ctx::create(const spb_scene_desc* s, Factor* f, int dev) {
     TRY(c22_contrib.upload(codes));
     dd = DenseDev{n2, N, sigma0_tiles.p, L.p, LinvT.p, Y.p, flags.p, counter.p, info.p,
                   c22_tile_ptr.p, c22_ent_rc.p, c22_ent_ptr.p, c22_contrib.p, prox_w.p, prox_c.p, active.p};
+    // INT8 tensor-core trailing updates (k_cholesky_oz): per-row power-of-two
+    // bounds. |L_rc| <= sqrt(H_rr) (L L^T = H) and H_rr <= sigma0_rr + the
+    // C22 diagonal with EVERY proxy active, so 2^erow[r] > sqrt of that bound
+    // holds for every active set; padded rows carry the identity
+    oz = chol_int8_enabled();
+    if (oz) {
+      std::vector<double> hmax((size_t)N * 64, 1.0);
+      for (int r = 0; r < n2; ++r) hmax[r] = f->sigma0[(size_t)r * n2 + r];
+      for (int j = 0; j < P; ++j)
+        for (int a = 0; a < 4; ++a) {
+          const int l = pl[4 * j + a];
+          const double w = s->proxy_weights[4 * (size_t)j + a];
+          if (l >= 0 && l < n2) hmax[l] += s->proxy_stiffness[j] * (w * w);
+        }
+      std::vector<int> er((size_t)N * 64);
+      for (size_t r = 0; r < er.size(); ++r) {
+        int ex = 0;
+        std::frexp(std::sqrt(std::max(hmax[r], 1e-300)), &ex);  // sqrt = f 2^ex, f in [0.5, 1): < 2^ex
+        er[r] = ex;
+      }
+      TRY(erow.upload(er));
+      TRY(Lq.zeros((size_t)nt * 32768));
+      dd.erow = erow.p;
+      dd.Lq = Lq.p;
+    }
   }
   // colliders + metrics
   e_blocks = energy_blocks(ne);
@@ -715,7 +743,7 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
       launch_build_g(st, n2, f_tilde2.p, gb_ptr.p, gb_src.p, Gb.p, nbeta, P_, tets.p, x.p, active.p, target.p,
                      gc_ptr.p, gc_src.p, g.p, Y.p);
       // (4.3)+(4.5) H = sigma0 + C22, LL^T = H, y = L^-1 g (one persistent launch), u2 = L^-T y
-      launch_cholesky_tiles(st, dd, tasks.p, ntasks, chol_grid, true);
+      launch_cholesky(st, dd, tasks.p, ntasks, chol_grid, true, oz);
       launch_dense_backward(st, dd, xrows.p, u2.p, nullptr, true);
       // (4.6)-(4.7) sigma0 u2 once for both the f~2 upkeep and the residual.
       // In the last pass nothing downstream of the backward sweep needs f~2:
@@ -1610,7 +1638,7 @@ int32_t spb_ctx_bench_kernel(spb_ctx* cp, int32_t which, int32_t reps, double* m
     case 0:
       cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st);
       cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st);
-      spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid);
+      spb::launch_cholesky(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid, false, c->oz);
       break;
     case 1: spb::launch_dense_backward(c->st, c->dd, c->xrows.p, c->u2.p); break;
     case 2:
@@ -1750,7 +1778,7 @@ int32_t spb_ctx_bench_cholesky(spb_ctx* cp, int32_t reps, double* ms) {
     SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
     SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
     SPB_CUDA(cudaEventRecord(e0, c->st));
-    spb::launch_cholesky_tiles(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid);
+    spb::launch_cholesky(c->st, c->dd, c->tasks.p, c->ntasks, c->chol_grid, false, c->oz);
     SPB_CUDA(cudaEventRecord(e1, c->st));
     SPB_CUDA(cudaEventSynchronize(e1));
     float ms1;

@@ -47,7 +47,7 @@ int dense_tile_count(int N) { return N * (N + 1) / 2; }
 constexpr int SM_STAGES = NSTAGE * 2 * PTILE;
 constexpr int SM_SCR = SM_STAGES;
 constexpr int SM_BAR = SM_SCR + PTILE;  // in doubles (8-byte aligned)
-size_t cholesky_smem_bytes() { return sizeof(double) * (SM_BAR + 2 * NSTAGE + 4 + 1); }
+size_t cholesky_smem_bytes() { return sizeof(double) * (SM_BAR + 2 * NSTAGE + 4 + 1 + 2); }  // + INT8 path: accumulator barrier, TMEM slot
 
 struct CholSmem {
   double* stage0;
@@ -952,6 +952,390 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_ranks(const DenseRankJ
   cholesky_body<true>(job.d, job.tasks, job.ntasks);
 }
 
+// =====================================================================
+// Emulated-FP64 trailing updates on the INT8 tensor cores (tcgen05)
+// ---------------------------------------------------------------------
+// The left-looking accumulation S = sum_k L_ik L_jk^T is the FP64 work of the
+// factorization (m^3 / 3 flops). DMMA (mma.sync m8n8k4.f64) tops out at ~37
+// TF on B200; tcgen05 has no FP64 kind. Here every finalized L tile is also
+// stored as 8 base-2^7 digit planes (Ozaki-style splitting, int8): row r of
+// L is scaled by a power of two 2^erow[r] > max |L_r.| (bounded a priori by
+// sqrt(H_rr) >= |L_rc|, since L L^T = H), and
+//   L_rc / 2^e_r = d1 / 2^6 + d2 / 2^13 + ... + d8 / 2^55  (|d_p| <= 64).
+// The digit products d_p(L_ik) d_q(L_jk)^T are exact in int32 on
+// tcgen05.mma.kind::i8 (|sum| < 2^28 per product over any K of this
+// problem), accumulated in TMEM per shift group p + q, and converted to FP64
+// with exact power-of-two scales: an error ~1e-17 of sum |L_rk L_ck|,
+// below that of an FP64 FMA chain (tools/ozaki_probe.cu). Pairs with
+// p + q <= 9 (plus the even-p pairs of 10) are kept.
+//
+// MMA shape M = 128 (two stacked digit planes of L_ik: 2h+1, 2h+2), N = 128
+// (planes q, q+1 of L_jk, q odd), K = 32; per 64-deep k-step 20 MMAs
+// (1,280 tensor cycles against 4,096 for the 64^3 DMMA step). TMEM block
+// bi = (2h + 1 + q - 2) / 2 (128 columns, all 512 columns used): its
+// quadrant (lanes 0-63 | 64-127) x (cols 0-63 | 64-127) accumulates shift
+// b | b+1 / b+1 | b+2 with b = 2 + 2 bi.
+constexpr int NDIG = 8;
+constexpr int DPLANE = TS * TS;        // bytes per digit plane of a tile
+constexpr int DTILE = NDIG * DPLANE;   // 32 KB: the digits of one L tile
+
+__host__ __device__ __forceinline__ int kmaj_off(int r, int k) {
+  return ((r >> 3) * 4 + (k >> 4)) * 128 + (r & 7) * 16 + (k & 15);
+}
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  // no-swizzle K-major: 8-row x 16-byte core matrices, k-chunks 128 B apart
+  // (LBO), 8-row groups 512 B apart (SBO), sm_100 descriptor version 1
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+// instruction descriptor: D s32, A/B signed 8-bit, K-major, N = 128, M = 128
+constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void umma_i8(uint32_t dtmem, uint64_t ad, uint64_t bd, int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
+      "l"(ad), "l"(bd), "r"(OZ_IDESC), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&u)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15]),
+        "=r"(u[16]), "=r"(u[17]), "=r"(u[18]), "=r"(u[19]), "=r"(u[20]), "=r"(u[21]), "=r"(u[22]), "=r"(u[23]),
+        "=r"(u[24]), "=r"(u[25]), "=r"(u[26]), "=r"(u[27]), "=r"(u[28]), "=r"(u[29]), "=r"(u[30]), "=r"(u[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// digits of a swizzled FP64 tile (rows of block `rb`) into the tile's 8
+// planes in global memory; 4 consecutive columns (one 32-bit word per plane)
+// per work item, threads t0, t0 + nt, ...
+__device__ __forceinline__ void tile_digits(const double* __restrict__ src, const int* __restrict__ erow, int rb,
+                                            signed char* __restrict__ dst, int t0, int nt) {
+  for (int w = t0; w < TS * TS / 4; w += nt) {
+    const int r = w >> 4, c0 = (w & 15) * 4;
+    const int e = erow[rb * TS + r];
+    uint32_t word[NDIG];
+#pragma unroll
+    for (int p = 0; p < NDIG; ++p) word[p] = 0u;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      double x = ldexp(src[swz(r, c0 + cc)], -e);
+      double dd = rint(x * 64.0);
+      word[0] |= (uint32_t)(uint8_t)(int8_t)dd << (8 * cc);
+      x = x * 64.0 - dd;
+#pragma unroll
+      for (int p = 1; p < NDIG; ++p) {
+        x *= 128.0;
+        dd = rint(x);
+        word[p] |= (uint32_t)(uint8_t)(int8_t)dd << (8 * cc);
+        x -= dd;
+      }
+    }
+    const int off = kmaj_off(r, c0);
+#pragma unroll
+    for (int p = 0; p < NDIG; ++p) *reinterpret_cast<uint32_t*>(dst + p * DPLANE + off) = word[p];
+  }
+}
+
+// One 64-deep k-step of S += L_a L_b^T from their digit planes in smem
+// (sa, sb: 32 KB each; sa == sb for the diagonal tasks). first: the task's
+// first k-step (the first MMA into each TMEM block overwrites).
+__device__ __forceinline__ void oz_kstep(uint32_t tmem, const signed char* sa, const signed char* sb, bool first) {
+  const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+#pragma unroll
+  for (int h = 0; h < 4; ++h)
+#pragma unroll
+    for (int q = 1; q <= NDIG; q += 2) {
+      const int b = 2 * h + 1 + q;
+      if (b > 9) continue;
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk)
+        umma_i8(tmem + (uint32_t)((b - 2) / 2 * 128), umma_desc(a0 + 2 * h * DPLANE + kk * 256),
+                umma_desc(b0 + (q - 1) * DPLANE + kk * 256), (first && h == 0 && kk == 0) ? 0 : 1);
+    }
+}
+
+// TMEM accumulators -> acc -= 2^(e_r + e_c) S over the tile (all 8 consumer
+// warps; warp w reads TMEM lane quarter w % 4, column half w / 4); P: the
+// swizzled scratch tile. Leaves TMEM free (fenced, behind a consumer barrier).
+__device__ __forceinline__ void oz_epilogue(uint32_t tmem, Acc& acc, double* P, const int* __restrict__ erow,
+                                            int ib, int jb, int warp, int lane, int wr, int wc) {
+  const int qd = warp & 3, ch = warp >> 2;
+  const int r = (32 * qd + lane) & 63;
+  double v[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) v[c] = 0.0;
+#pragma unroll 1
+  for (int blk = 0; blk < 8; ++blk) {
+    uint32_t u[32];
+    tmem_ld32(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)((blk >> 1) * 128 + (blk & 1) * 64 + 32 * ch), u);
+    const int t = 2 + 2 * (blk >> 1) + (blk & 1) + (qd >= 2 ? 1 : 0);
+    const double w = __longlong_as_double((long long)(1023 - (7 * t - 2)) << 52);  // 2^-(7t-2), exact
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)u[c], w, v[c]);
+  }
+  tc_fence_before();
+  if (qd < 2) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) P[swz(r, 32 * ch + c)] = v[c];
+  }
+  cons_sync();
+  if (qd >= 2) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) P[swz(r, 32 * ch + c)] += v[c];
+  }
+  cons_sync();
+  acc_foreach(wr, wc, lane, [&](int mb, int nb, int rr, int cc) {
+    const int er = erow[ib * TS + rr];
+    const double2 pv = *reinterpret_cast<const double2*>(P + swz(rr, cc));
+    acc.c[mb][nb][0] -= ldexp(pv.x, er + erow[jb * TS + cc]);
+    acc.c[mb][nb][1] -= ldexp(pv.y, er + erow[jb * TS + cc + 1]);
+  });
+  cons_sync();  // P (the scratch tile) is free again
+}
+
+// The left-looking tile Cholesky of cholesky_body with the k-loop on the INT8
+// tensor cores (single GPU; the tile-cyclic MULTI path stays on DMMA). Task
+// list, flags, diagonal chain, RHS row and finalizes are those of
+// cholesky_body; what changes:
+//   * the producer streams the 32 KB digit tiles of L_ik / L_jk instead of
+//     the FP64 tiles for the k-loop (RHS row and finalize inputs stay FP64);
+//   * consumer warp 0, lane 0 issues the 20 MMAs per k-step and releases
+//     the stage with tcgen05.commit (8 arrivals: the empty barriers keep
+//     their 8-warp count); the last k-step commits to the accumulator barrier;
+//   * every finalized L tile (regular tiles and the sub-diagonal tile the
+//     diagonal task finalizes) also gets its digit planes before its flag.
+__global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const int2* __restrict__ tasks, int ntasks) {
+  extern __shared__ __align__(1024) double smd[];
+  CholSmem sm;
+  sm.stage0 = smd;
+  sm.scratch = smd + SM_SCR;
+  sm.full = reinterpret_cast<unsigned long long*>(smd + SM_BAR);
+  sm.empty = sm.full + NSTAGE;
+  sm.tfull = sm.empty + NSTAGE;
+  sm.tempty = sm.tfull + 2;
+  sm.task = reinterpret_cast<int*>(sm.tempty + 2);
+  unsigned long long* accf = reinterpret_cast<unsigned long long*>(sm.task + 2);  // 8-byte aligned (task: 2 ints)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool producer = warp == 8;
+  const int wr = warp >> 2, wc = warp & 3;
+  const int N = d.N;
+  const int ntiles = N * (N + 1) / 2;
+  if (tid == 0) pdl_trigger();
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], NCONS / 32);
+    }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&sm.tfull[k], 1);
+      mbar_init(&sm.tempty[k], NCONS / 32);
+    }
+    mbar_init(accf, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  int it = 0;
+  if (producer) {
+    auto fill = [&](const void* a, const void* b, int slot_a, int abytes = TILE_BYTES) {
+      const int s = it % NSTAGE;
+      if (lane == 0) {
+        mbar_wait(&sm.empty[s], ((it / NSTAGE) & 1) ^ 1);
+        mbar_expect_tx(&sm.full[s], abytes + (b ? TILE_BYTES : 0));
+        bulk_g2s(sm.slot(s, slot_a), a, abytes, &sm.full[s]);
+        if (b) bulk_g2s(sm.slot(s, 1), b, TILE_BYTES, &sm.full[s]);
+      }
+      __syncwarp();
+      ++it;
+    };
+    auto wait_ready = [&](const int* f, int v) {
+      if (lane == 0) poll_flag<false>(f, v);
+      __syncwarp();
+    };
+    auto tile_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), r == c + 1 ? 2 : 1); };
+    for (int use = 0;; ++use) {
+      const int k2 = use & 1;
+      int task = 0;
+      if (lane == 0) {
+        task = atomicAdd(d.counter, 1);
+        mbar_wait(&sm.tempty[k2], ((use >> 1) & 1) ^ 1);
+        sm.task[k2] = task;
+        mbar_arrive(&sm.tfull[k2]);
+      }
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task >= ntasks) break;
+      const int2 ij = tasks[task];
+      const int i = ij.x, j = ij.y;
+      const bool rhs = (i == N);
+      const double* src = rhs ? d.Y + (size_t)j * TILE : d.sigma0 + (size_t)tidx(i, j) * TILE;
+      if (rhs && lane == 0) {
+        pdl_wait();
+        fence_proxy_async_global();
+      }
+      fill(src, nullptr, 0, rhs ? RHS_BYTES : TILE_BYTES);
+      if (i == j) {
+        for (int k = 0; k < j - 1; ++k) {
+          tile_ready(j, k);
+          fill(d.Lq + (size_t)tidx(j, k) * DTILE, nullptr, 0);
+        }
+        if (j > 0) {
+          wait_ready(d.flags + tidx(j, j - 1), 1);
+          fill(d.L + (size_t)tidx(j, j - 1) * TILE, nullptr, 0);
+          wait_ready(d.flags + tidx(j - 1, j - 1), 1);
+          fill(d.LinvT + (size_t)(j - 1) * TILE, nullptr, 1);
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");
+      } else {
+        for (int k = 0; k < j; ++k) {
+          if (rhs) wait_ready(d.flags + ntiles + k, 1);
+          else tile_ready(i, k);
+          tile_ready(j, k);
+          if (rhs) fill(d.Y + (size_t)k * TILE, d.L + (size_t)tidx(j, k) * TILE, 0, RHS_BYTES);
+          else fill(d.Lq + (size_t)tidx(i, k) * DTILE, d.Lq + (size_t)tidx(j, k) * DTILE, 0);
+        }
+        if (i != j + 1 || rhs) {
+          wait_ready(d.flags + tidx(j, j), 1);
+          fill(d.LinvT + (size_t)j * TILE, nullptr, 1);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------------------------------------------------- consumers
+  int acc_phase = 0;
+  for (int use = 0;; ++use) {
+    const int k2 = use & 1;
+    mbar_wait(&sm.tfull[k2], (use >> 1) & 1);
+    const int task = sm.task[k2];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.tempty[k2]);
+    if (task >= ntasks) break;
+    const int2 ij = tasks[task];
+    const int i = ij.x, j = ij.y;
+    const bool rhs = (i == N);
+    int* myflag = d.flags + (rhs ? ntiles + j : tidx(i, j));
+    Acc acc;
+    int s = it % NSTAGE;
+    mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+    if (!rhs && d.c22_tile_ptr && d.c22_tile_ptr[tidx(i, j)] < d.c22_tile_ptr[tidx(i, j) + 1]) {
+      add_c22(d, tidx(i, j), sm.slot(s, 0));
+      cons_sync();
+    }
+    smem_to_acc(acc, sm.slot(s, 0), wr, wc, lane);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
+    ++it;
+    const int nk = (i == j) ? j - 1 : j;
+    if (rhs) {
+      for (int k = 0; k < nk; ++k) {
+        s = it % NSTAGE;
+        mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+        if (wr == 0) mma_abt_m8<true>(acc, sm.slot(s, 0), sm.slot(s, 1), wc, lane);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        ++it;
+      }
+    } else if (nk > 0) {
+      // ---- the k-loop on the tensor cores: one thread issues, commits free the stages
+      if (tid == 0) {
+        for (int k = 0; k < nk; ++k) {
+          s = (it + k) % NSTAGE;
+          mbar_wait(&sm.full[s], ((it + k) / NSTAGE) & 1);
+          tc_fence_after();
+          const signed char* sa = reinterpret_cast<const signed char*>(sm.slot(s, 0));
+          const signed char* sb = (i == j) ? sa : reinterpret_cast<const signed char*>(sm.slot(s, 1));
+          oz_kstep(tmem, sa, sb, k == 0);
+#pragma unroll
+          for (int w = 0; w < NCONS / 32; ++w) umma_commit(&sm.empty[s]);  // 8 arrivals when the MMAs are done
+        }
+        umma_commit(accf);
+      }
+      it += nk;
+      mbar_wait(accf, acc_phase);
+      acc_phase ^= 1;
+      tc_fence_after();
+      oz_epilogue(tmem, acc, sm.scratch, d.erow, i, j, warp, lane, wr, wc);
+    }
+    if (i == j && j > 0) {
+      // ---- finalize the sub-diagonal tile on the chain (as cholesky_body),
+      // plus its digit planes before it is released (inside the factorization)
+      const int sa = it % NSTAGE;
+      mbar_wait(&sm.full[sa], (it / NSTAGE) & 1);
+      ++it;
+      const int sb = it % NSTAGE;
+      mbar_wait(&sm.full[sb], (it / NSTAGE) & 1);
+      ++it;
+      TriAcc out;
+      mma_ab_upper(out, sm.slot(sa, 0), sm.slot(sb, 1), warp, lane);
+      cons_sync();
+      double* scratch = sm.scratch;
+      tri_to_swz(out, scratch, warp, lane);
+      tri_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, warp, lane);
+      cons_sync();
+      tile_digits(scratch, d.erow, j, d.Lq + (size_t)tidx(j, j - 1) * DTILE, tid, NCONS);
+      fence_proxy_async_global();
+      if (lane == 0) {
+        mbar_arrive(&sm.empty[sa]);
+        mbar_arrive(&sm.empty[sb]);
+      }
+    }
+    if (i == j) {
+      potrf_blocked_tile<false>(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
+                                d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane, d.peers,
+                                j > 0 ? sm.scratch : nullptr, j > 0 ? d.flags + tidx(j, j - 1) : nullptr,
+                                j > 0 ? tidx(j, j - 1) : 0);
+    } else if (i == j + 1 && !rhs) {
+      acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
+    } else {
+      acc_to_swz(acc, sm.scratch, wr, wc, lane);
+      cons_sync();
+      s = it % NSTAGE;
+      mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+      TriAcc out;
+      mma_ab_upper(out, sm.scratch, sm.slot(s, 1), warp, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      ++it;
+      double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
+      tri_to_swz(out, dst, warp, lane);
+      if (!rhs) {
+        cons_sync();  // every warp is done reading the scratch tile
+        tri_to_swz(out, sm.scratch, warp, lane);
+        cons_sync();
+        tile_digits(sm.scratch, d.erow, i, d.Lq + (size_t)tidx(i, j) * DTILE, tid, NCONS);
+      }
+    }
+    fence_proxy_async_smem();
+    fence_proxy_async_global();
+    fence_tile_stores<false>();
+    cons_sync();
+    if (tid == 0) st_release(myflag, 1);
+    if (i == j) asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");
+  }
+  // consumers: release TMEM (every MMA of this CTA has been waited on)
+  tc_fence_before();
+  cons_sync();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 // u = L^-T y, block rows from the bottom: x_j = (y_j - sum_{i>j} x_i L_ij) W_j
 // with W_j = inv(L_jj)^T (x_j, y_j: 3 x 64 row blocks; x_i L_ij: 3x64 * 64x64).
 // CTA b owns block j = N-1-b and only waits on lower CTA indices.
@@ -1496,6 +1880,30 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
     return;
   }
   k_cholesky_tiles<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
+}
+
+void launch_cholesky(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid, bool pdl,
+                     bool int8) {
+  if (!int8) {
+    launch_cholesky_tiles(st, d, tasks, ntasks, grid, pdl);
+    return;
+  }
+  static bool attr = false;
+  size_t smem = cholesky_smem_bytes();
+  if (!attr) {
+    cudaFuncSetAttribute(k_cholesky_oz, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (pdl) {
+    launch_pdl(k_cholesky_oz, dim3(grid), dim3(NTHREADS), smem, st, d, tasks, ntasks);
+    return;
+  }
+  k_cholesky_oz<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
+}
+
+bool chol_int8_enabled() {
+  static const bool on = !(getenv("SPB_CHOL_INT8") && getenv("SPB_CHOL_INT8")[0] == '0');
+  return on;
 }
 
 void launch_cholesky_ranks(cudaStream_t st, const DenseRankJob* jobs, int P, int grid) {

@@ -74,6 +74,11 @@ struct DenseDev {
   const uint8_t* active;
   unsigned long long* trace;  // optional: per task {claim, k-loop done, finalize done, sm}
   DensePeers peers;           // replicas this rank also writes (tile-cyclic mode)
+  // emulated-FP64 trailing updates on the INT8 tensor cores (k_cholesky_oz):
+  // per row a power-of-two bound 2^erow[r] > max |L_r.|, and per L tile its 8
+  // base-2^7 digit planes (int8, canonical K-major tcgen05 layout, 32 KB)
+  const int* erow;
+  signed char* Lq;
 };
 // one rank's share of a tile-cyclic factorization: its replica, peers and task list
 struct DenseRankJob {
@@ -85,6 +90,11 @@ int dense_tile_count(int N);
 size_t cholesky_smem_bytes();
 // pdl: launched programmatically behind build_g (only the RHS row waits for it)
 void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid, bool pdl = false);
+// the frame's factorization: k_cholesky_oz (INT8 tensor-core k-loop) when
+// int8, else k_cholesky_tiles (FP64 DMMA)
+void launch_cholesky(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid, bool pdl, bool int8);
+// SPB_CHOL_INT8 (default 1): contexts factor with the INT8 tensor-core path
+bool chol_int8_enabled();
 std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead);
 // P ranks (real: one job per process, P = 1 per launch; emulated: one launch
 // over all ranks' replicas, CTA b serving rank b % P)
