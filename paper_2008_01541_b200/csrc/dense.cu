@@ -349,6 +349,10 @@ __device__ __forceinline__ void add_c22(const DenseDev& d, int tile, double* S) 
   }
 }
 
+// digit planes of a swizzled FP64 tile (INT8 tensor-core path, defined below)
+__device__ __forceinline__ void tile_digits(const double* __restrict__ src, const int* __restrict__ erow, int rb,
+                                            signed char* __restrict__ dst, int t0, int nt, int r0 = 0, int r1 = 64);
+
 // ------------------------------------------------ diagonal tile factorization
 // Blocked factorization of the augmented 128 x 64 panel [A; I] held in shared
 // memory (row stride LSP, conflict-free DMMA fragments): for each 16-column
@@ -517,7 +521,8 @@ template <bool MULTI>
 // peers' replicas at rel_idx) by warp 7 while warp 0 factors the first block.
 __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double* gL, double* gLinvT, int j,
                                    int* info, int* flag, int wr, int wc, int lane, const DensePeers& pr,
-                                   const double* upd, int* rel_flag = nullptr, int rel_idx = 0) {
+                                   const double* upd, int* rel_flag = nullptr, int rel_idx = 0,
+                                   signed char* dig_out = nullptr, const int* erow = nullptr) {
   const int tid = threadIdx.x, warp = tid >> 5;
   POTRF_MARK(0)
   const int g = lane >> 2, t = lane & 3;
@@ -607,7 +612,15 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
       }
       potrf_diag16(S, DT, o, j, info, lane);
     } else {
-      if (kb == 0 && rel_flag && warp == NCONS / 32 - 1 && lane == 0) {
+      if (kb < 2 && rel_flag && dig_out) {
+        // INT8 path: the sub-diagonal tile's digit planes, written by warps
+        // 1-7 while warp 0 pivots blocks 0 and 1 (half the rows each), precede
+        // its release (the partial (j+1, j) that reads them has ~5 us of slack)
+        tile_digits(upd, erow, j, dig_out, tid - 32, NCONS - 32, 32 * kb, 32 * kb + 32);
+        fence_proxy_async_global();
+        if (kb == 1) asm volatile("bar.sync 4, %0;" ::"n"(NCONS - 32) : "memory");
+      }
+      if (kb == (dig_out ? 1 : 0) && rel_flag && warp == NCONS / 32 - 1 && lane == 0) {
         // every thread's stores of the tile precede the barriers above
         fence_tile_stores<MULTI>();
         st_release(rel_flag, 2);
@@ -982,6 +995,8 @@ constexpr int DTILE = NDIG * DPLANE;   // 32 KB: the digits of one L tile
 __host__ __device__ __forceinline__ int kmaj_off(int r, int k) {
   return ((r >> 3) * 4 + (k >> 4)) * 128 + (r & 7) * 16 + (k & 15);
 }
+// 2^k as a double, exact for -1022 <= k <= 1023 (bit construction)
+__device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(k + 1023) << 52); }
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
   // no-swizzle K-major: 8-row x 16-byte core matrices, k-chunks 128 B apart
   // (LBO), 8-row groups 512 B apart (SBO), sm_100 descriptor version 1
@@ -1018,16 +1033,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&u)[32]) {
 // planes in global memory; 4 consecutive columns (one 32-bit word per plane)
 // per work item, threads t0, t0 + nt, ...
 __device__ __forceinline__ void tile_digits(const double* __restrict__ src, const int* __restrict__ erow, int rb,
-                                            signed char* __restrict__ dst, int t0, int nt) {
-  for (int w = t0; w < TS * TS / 4; w += nt) {
+                                            signed char* __restrict__ dst, int t0, int nt, int r0, int r1) {
+  for (int w = r0 * 16 + t0; w < r1 * 16; w += nt) {
     const int r = w >> 4, c0 = (w & 15) * 4;
-    const int e = erow[rb * TS + r];
+    const double sc = pow2i(-erow[rb * TS + r]);  // exact scaling (no ldexp call)
     uint32_t word[NDIG];
 #pragma unroll
     for (int p = 0; p < NDIG; ++p) word[p] = 0u;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
-      double x = ldexp(src[swz(r, c0 + cc)], -e);
+      double x = src[swz(r, c0 + cc)] * sc;
       double dd = rint(x * 64.0);
       word[0] |= (uint32_t)(uint8_t)(int8_t)dd << (8 * cc);
       x = x * 64.0 - dd;
@@ -1096,8 +1111,8 @@ __device__ __forceinline__ void oz_epilogue(uint32_t tmem, Acc& acc, double* P, 
   acc_foreach(wr, wc, lane, [&](int mb, int nb, int rr, int cc) {
     const int er = erow[ib * TS + rr];
     const double2 pv = *reinterpret_cast<const double2*>(P + swz(rr, cc));
-    acc.c[mb][nb][0] -= ldexp(pv.x, er + erow[jb * TS + cc]);
-    acc.c[mb][nb][1] -= ldexp(pv.y, er + erow[jb * TS + cc + 1]);
+    acc.c[mb][nb][0] -= pv.x * pow2i(er + erow[jb * TS + cc]);
+    acc.c[mb][nb][1] -= pv.y * pow2i(er + erow[jb * TS + cc + 1]);
   });
   cons_sync();  // P (the scratch tile) is free again
 }
@@ -1168,7 +1183,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
       if (lane == 0) poll_flag<false>(f, v);
       __syncwarp();
     };
-    auto tile_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), r == c + 1 ? 2 : 1); };
+    // flags in this kernel: a regular tile (r >= c + 2) is final in FP64 at 1
+    // and has its digit planes at 2; a sub-diagonal tile (c + 1, c) is a
+    // partial sum at 1 and final (FP64) at 2 -- no task ever reads its digits
+    // (the k-step k = j - 1 of every task runs in FP64, see below)
+    auto fp64_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), r == c + 1 ? 2 : 1); };
+    auto digits_ready = [&](int r, int c) { wait_ready(d.flags + tidx(r, c), 2); };
+    // Batched readiness: the warp loads the flags of 16 k-steps at once (lanes
+    // 0-15: tile (ra, k), lanes 16-31: tile (rb, k)); one fence then covers
+    // every flag observed ready, and only the k-steps whose flags were not
+    // yet set are polled one by one. (A per-k-step poll is two dependent L2
+    // round trips + fences: longer than the INT8 k-step itself.)
+    // digits: both tiles' digit planes (flag 2; regular tiles only); else
+    // FP64 readiness (ra = N: the RHS row, flags ntiles + k)
+    auto ready_mask = [&](int ra, int rb, int k0, int kmax, bool digits) -> unsigned {
+      const int kk = k0 + (lane & 15);
+      bool ok = true;
+      if (kk < kmax) {
+        const int r = lane < 16 ? ra : rb;
+        const int* f = (r == N) ? d.flags + ntiles + kk : d.flags + tidx(r, kk);
+        const int v = digits ? 2 : ((r != N && r == kk + 1) ? 2 : 1);
+        ok = ld_relaxed(f) >= v;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) {
+        fence_acq_rel_gpu();
+        fence_proxy_async_global();
+      }
+      __syncwarp();
+      return (m & 0xFFFFu) & (m >> 16);  // bit l: both tiles of k-step k0 + l ready
+    };
     for (int use = 0;; ++use) {
       const int k2 = use & 1;
       int task = 0;
@@ -1190,8 +1234,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
       }
       fill(src, nullptr, 0, rhs ? RHS_BYTES : TILE_BYTES);
       if (i == j) {
+        unsigned rm = 0;
         for (int k = 0; k < j - 1; ++k) {
-          tile_ready(j, k);
+          if ((k & 15) == 0) rm = ready_mask(j, j, k, j - 1, true);
+          if (!((rm >> (k & 15)) & 1u)) digits_ready(j, k);
           fill(d.Lq + (size_t)tidx(j, k) * DTILE, nullptr, 0);
         }
         if (j > 0) {
@@ -1202,12 +1248,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
         }
         asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");
       } else {
-        for (int k = 0; k < j; ++k) {
-          if (rhs) wait_ready(d.flags + ntiles + k, 1);
-          else tile_ready(i, k);
-          tile_ready(j, k);
+        unsigned rm = 0;
+        // every matrix task takes its last k-step (k = j - 1: the fresh
+        // sub-diagonal L(j, j - 1) and L(i, j - 1), at the diagonal chain) in
+        // FP64 from the FP64 tiles: no task waits for digit planes of a tile
+        // finalized in the last column (RHS row: FP64 throughout)
+        const int kq = rhs ? j : j - 1;
+        for (int k = 0; k < kq; ++k) {
+          if ((k & 15) == 0) rm = ready_mask(i, j, k, kq, !rhs);
+          if (!((rm >> (k & 15)) & 1u)) {
+            if (rhs) {
+              wait_ready(d.flags + ntiles + k, 1);
+              fp64_ready(j, k);
+            } else {
+              digits_ready(i, k);
+              digits_ready(j, k);
+            }
+          }
           if (rhs) fill(d.Y + (size_t)k * TILE, d.L + (size_t)tidx(j, k) * TILE, 0, RHS_BYTES);
           else fill(d.Lq + (size_t)tidx(i, k) * DTILE, d.Lq + (size_t)tidx(j, k) * DTILE, 0);
+        }
+        if (!rhs && j > 0) {
+          fp64_ready(i, j - 1);
+          fp64_ready(j, j - 1);
+          fill(d.L + (size_t)tidx(i, j - 1) * TILE, d.L + (size_t)tidx(j, j - 1) * TILE, 0);
         }
         if (i != j + 1 || rhs) {
           wait_ready(d.flags + tidx(j, j), 1);
@@ -1219,6 +1283,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
   }
   // ---------------------------------------------------------- consumers
   int acc_phase = 0;
+  unsigned long long t_claim = 0, t_kdone = 0, t_fin = 0;
   for (int use = 0;; ++use) {
     const int k2 = use & 1;
     mbar_wait(&sm.tfull[k2], (use >> 1) & 1);
@@ -1230,6 +1295,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
     const int i = ij.x, j = ij.y;
     const bool rhs = (i == N);
     int* myflag = d.flags + (rhs ? ntiles + j : tidx(i, j));
+    if (d.trace && tid == 0) t_claim = globaltimer();
     Acc acc;
     int s = it % NSTAGE;
     mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
@@ -1242,7 +1308,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);
     ++it;
-    const int nk = (i == j) ? j - 1 : j;
+    const int nk = rhs ? j : j - 1;  // digit-plane k-steps (RHS: FP64 k-steps)
     if (rhs) {
       for (int k = 0; k < nk; ++k) {
         s = it % NSTAGE;
@@ -1252,26 +1318,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
         if (lane == 0) mbar_arrive(&sm.empty[s]);
         ++it;
       }
-    } else if (nk > 0) {
+    }
+    if (!rhs && nk > 0) {
       // ---- the k-loop on the tensor cores: one thread issues, commits free the stages
-      if (tid == 0) {
+      if (warp == 0) {
+        // the whole warp waits (no divergent spin beside the issuing lane);
+        // lane 0 issues
         for (int k = 0; k < nk; ++k) {
           s = (it + k) % NSTAGE;
           mbar_wait(&sm.full[s], ((it + k) / NSTAGE) & 1);
           tc_fence_after();
-          const signed char* sa = reinterpret_cast<const signed char*>(sm.slot(s, 0));
-          const signed char* sb = (i == j) ? sa : reinterpret_cast<const signed char*>(sm.slot(s, 1));
-          oz_kstep(tmem, sa, sb, k == 0);
+          if (lane == 0) {
+            const signed char* sa = reinterpret_cast<const signed char*>(sm.slot(s, 0));
+            const signed char* sb = (i == j) ? sa : reinterpret_cast<const signed char*>(sm.slot(s, 1));
+            oz_kstep(tmem, sa, sb, k == 0);
 #pragma unroll
-          for (int w = 0; w < NCONS / 32; ++w) umma_commit(&sm.empty[s]);  // 8 arrivals when the MMAs are done
+            for (int w = 0; w < NCONS / 32; ++w) umma_commit(&sm.empty[s]);  // 8 arrivals when the MMAs are done
+            if (k == nk - 1) umma_commit(accf);
+          }
+          __syncwarp();
         }
-        umma_commit(accf);
       }
       it += nk;
       mbar_wait(accf, acc_phase);
       acc_phase ^= 1;
       tc_fence_after();
       oz_epilogue(tmem, acc, sm.scratch, d.erow, i, j, warp, lane, wr, wc);
+    }
+    if (!rhs && i != j && j > 0) {
+      // ---- the last k-step (k = j - 1) in FP64 on DMMA
+      s = it % NSTAGE;
+      mbar_wait(&sm.full[s], (it / NSTAGE) & 1);
+      mma_abt<true>(acc, sm.slot(s, 0), sm.slot(s, 1), wr, wc, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s]);
+      ++it;
     }
     if (i == j && j > 0) {
       // ---- finalize the sub-diagonal tile on the chain (as cholesky_body),
@@ -1288,19 +1369,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
       double* scratch = sm.scratch;
       tri_to_swz(out, scratch, warp, lane);
       tri_to_swz(out, d.L + (size_t)tidx(j, j - 1) * TILE, warp, lane);
-      cons_sync();
-      tile_digits(scratch, d.erow, j, d.Lq + (size_t)tidx(j, j - 1) * DTILE, tid, NCONS);
+      // its digit planes are written inside the factorization, off the pivot chain
       fence_proxy_async_global();
       if (lane == 0) {
         mbar_arrive(&sm.empty[sa]);
         mbar_arrive(&sm.empty[sb]);
       }
     }
+    if (d.trace && tid == 0) t_kdone = globaltimer();
     if (i == j) {
       potrf_blocked_tile<false>(acc, sm.stage0, sm.stage0 + 128 * LSP, d.L + (size_t)tidx(j, j) * TILE,
                                 d.LinvT + (size_t)j * TILE, j, d.info, myflag, wr, wc, lane, d.peers,
                                 j > 0 ? sm.scratch : nullptr, j > 0 ? d.flags + tidx(j, j - 1) : nullptr,
                                 j > 0 ? tidx(j, j - 1) : 0);
+      if (d.trace && tid == 0) t_fin = globaltimer();  // the factorization (and the diagonal's release) is done
     } else if (i == j + 1 && !rhs) {
       acc_to_swz(acc, d.L + (size_t)tidx(i, j) * TILE, wr, wc, lane);
     } else {
@@ -1316,17 +1398,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cholesky_oz(DenseDev d, const i
       double* dst = rhs ? d.Y + (size_t)j * TILE : d.L + (size_t)tidx(i, j) * TILE;
       tri_to_swz(out, dst, warp, lane);
       if (!rhs) {
-        cons_sync();  // every warp is done reading the scratch tile
+        // the FP64 tile is final (flag 1: the FP64 last k-steps of column i
+        // and the dense backward read it), then its digit planes (flag 2)
+        fence_proxy_async_global();
+        fence_tile_stores<false>();
+        cons_sync();  // also: every warp is done reading the scratch tile
+        if (tid == 0) st_release(myflag, 1);
         tri_to_swz(out, sm.scratch, warp, lane);
         cons_sync();
         tile_digits(sm.scratch, d.erow, i, d.Lq + (size_t)tidx(i, j) * DTILE, tid, NCONS);
       }
     }
+    if (d.trace && tid == 0 && i != j) t_fin = globaltimer();
     fence_proxy_async_smem();
     fence_proxy_async_global();
     fence_tile_stores<false>();
     cons_sync();
-    if (tid == 0) st_release(myflag, 1);
+    if (tid == 0) {
+      // regular tiles: 2 = digit planes written too; partials, diagonals, RHS: 1
+      st_release(myflag, (!rhs && i >= j + 2) ? 2 : 1);
+      if (d.trace) {
+        unsigned long long* tr = d.trace + 4 * (size_t)task;
+        tr[0] = t_claim;
+        tr[1] = t_kdone;
+        tr[2] = globaltimer();
+        tr[3] = t_fin;
+      }
+    }
     if (i == j) asm volatile("bar.sync 2, %0;" ::"n"(NTHREADS) : "memory");
   }
   // consumers: release TMEM (every MMA of this CTA has been waited on)
