@@ -147,19 +147,56 @@ def measured_hbm_peak():
         return 6552.3, "fallback (no MEASURED_PEAKS.json on this box)"
 
 
-def committed_traffic(config: str, m: int):
-    """dram__bytes_read.sum + dram__bytes_write.sum of one k_cholesky_tiles
-    launch of THIS config (dense order m) from the newest committed
-    `ncu --set full` capture (profiles/r*_cholesky_traffic_<config>.json);
-    None when no capture of this config is committed."""
+def committed_traffic(config: str, m: int, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one launch of THIS
+    factorization kernel on THIS config (dense order m) from the newest
+    committed `ncu --set full` capture (profiles/r*_cholesky_traffic_<config>.json);
+    None when no capture of this kernel and config is committed."""
     caps = sorted((ROOT / "profiles").glob(f"r*_cholesky_traffic_{config}.json"))
     if config == "cfg3":
         caps = sorted(caps + sorted((ROOT / "profiles").glob("r01_cholesky_traffic.json")))
     for cap in reversed(caps):
         js = json.loads(cap.read_text())
-        if int(js.get("m", m)) == m:
+        if int(js.get("m", 6197)) == m and js.get("kernel") == kernel:
             return js.get("traffic_bytes"), f"profiles/{cap.name} (ncu --set full, one launch)"
     return None, None
+
+
+def int8_ops_per_launch(m: int) -> float:
+    """Tensor-core INT8 ops one k_cholesky_oz launch executes: every matrix
+    task (i, j) runs j - 1 digit-plane k-steps (its k = j - 1 step is FP64),
+    each 20 tcgen05.mma.kind::i8 of 128 x 128 x 32 (2 ops per MAC)."""
+    N = (m + 63) // 64
+    steps = sum((N - j) * max(j - 1, 0) for j in range(N))
+    return steps * 20 * 2.0 * 128 * 128 * 32
+
+
+def cholesky_roofline(int8: bool, m: int, ms: float, fp64_equiv_tf: float, fp64_peak: float, traffic, traffic_src):
+    """The dominant kernel's roofline entry. DMMA path: FP64 flops (m^3/3)
+    against live cuBLAS DGEMM. INT8 path (emulated FP64): the int8 tensor ops
+    it executes against the INT8 dense tensor rate, taken as 2x the measured
+    bf16 GEMM burst of MEASURED_PEAKS.json (the tensor core's int8/fp8 rate is
+    twice its bf16 rate per MMA); the FP64-equivalent rate (m^3/3 per launch)
+    is reported beside it against the DGEMM peak."""
+    base = {"traffic": traffic, "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
+            "flops_per_launch": m ** 3 / 3.0, "fp64_equivalent_tflops": fp64_equiv_tf,
+            "fp64_dgemm_peak_tflops": fp64_peak,
+            "fp64_peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (MEASURED_PEAKS.json has no FP64)"}
+    if not int8:
+        return {"bound": "tensor", "kernel": "k_cholesky_tiles (FP64 DMMA)", "achieved": fp64_equiv_tf,
+                "peak": fp64_peak, "unit": "TFLOP/s", "frac": fp64_equiv_tf / fp64_peak,
+                "peak_source": base["fp64_peak_source"], **base}
+    try:
+        bf16 = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+        src = "2 x MEASURED_PEAKS.json bf16_tflops (burst, of measured): the int8 dense tensor rate"
+    except Exception:
+        bf16, src = 2250.0, "2 x the 2.25 PFLOP/s nominal bf16 dense rate (of fallback)"
+    ops = int8_ops_per_launch(m)
+    tops = ops / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "kernel": "k_cholesky_oz (INT8 tcgen05.mma, emulated FP64 trailing updates)",
+            "achieved": tops, "peak": 2.0 * bf16, "unit": "TOPS (int8)", "frac": tops / (2.0 * bf16),
+            "peak_source": src, "int8_ops_per_launch": ops,
+            "fp64_equivalent_vs_dgemm": fp64_equiv_tf / fp64_peak, **base}
 
 
 def build_sim(config: str, outer: int, inner: int, collider: str = "plane"):
@@ -400,7 +437,9 @@ def run_b200(args):
             dist.destroy_process_group()
         return
     fp64_peak = measure_fp64_peak()
-    traffic, traffic_src = committed_traffic(args.config, m)
+    kind = ctypes.c_int32(0)
+    _native.check(lib.spb_ctx_cholesky_kind(ds.handle, ctypes.byref(kind)))
+    traffic, traffic_src = committed_traffic(args.config, m, "k_cholesky_oz" if kind.value else "k_cholesky_tiles")
     # per-piece graph-replay times -> achieved HBM GB/s of the solves (north_star (4))
     kms = {}
     for name, which in (("cholesky", 0), ("dense_backward", 1), ("sigma0_gemv", 2), ("sparse_forward", 3),
@@ -418,6 +457,7 @@ def run_b200(args):
     t_fp64 = chol_flops / (fp64_peak * 1e12) * 1e3
     t_hbm = bytes_frame / (hbm_peak * 1e9) * 1e3
     achieved = chol_flops / (chol.value * 1e-3) / 1e12
+    roofline = cholesky_roofline(bool(kind.value), m, chol.value, achieved, fp64_peak, traffic, traffic_src)
     line = {
         "metric": metric_for(args.config),
         "value": replica_throughput(world, ms_frame), "unit": "frames/s", "n_gpus": world, "steps": args.steps,
@@ -428,11 +468,7 @@ def run_b200(args):
         "cholesky_fp64_tflops": achieved, "cholesky_ms": chol.value,
         "phases_ms": {"local_alpha+forces": phase[0], "forward_sweep": phase[1], "inner_loop": phase[2],
                       "backward_sweep": phase[3], "metrics": phase[4]},
-        "roofline": {"bound": "tensor", "kernel": "k_cholesky_tiles (FP64 DMMA)", "achieved": achieved,
-                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
-                     "traffic_unit": "bytes per launch", "traffic_source": traffic_src,
-                     "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (MEASURED_PEAKS.json has no FP64)",
-                     "flops_per_launch": chol_flops},
+        "roofline": roofline,
         "kernels_ms": kms,
         "hbm_gbs": {"sparse_forward": gbs(panel_bytes, kms["sparse_forward"]),
                     "sparse_backward": gbs(panel_bytes, kms["sparse_backward"]),

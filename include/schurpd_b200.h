@@ -242,6 +242,10 @@ int32_t spb_ctx_bench(spb_ctx *ctx, const spb_step_config *cfg, int32_t frames, 
                       double *phase_ms /* [6]: local, forward, inner-detect, dense, backward, metrics */);
 /* Diagnostics: per-task timestamps of one tile-Cholesky launch (see context.cu). */
 int32_t spb_ctx_trace_cholesky(spb_ctx *ctx, uint64_t *out, int32_t *tasks_out, int32_t *ntasks);
+/* Which factorization the context runs: 1 = trailing updates on the INT8
+ * tensor cores (emulated FP64, k_cholesky_oz), 0 = FP64 DMMA (k_cholesky_tiles;
+ * SPB_CHOL_INT8=0 at context creation). */
+int32_t spb_ctx_cholesky_kind(spb_ctx *ctx, int32_t *kind);
 /* Cholesky-only timing on the context's current H (tile kernel), ms per launch. */
 int32_t spb_ctx_bench_cholesky(spb_ctx *ctx, int32_t reps, double *ms);
 /* Diagnostics: per-block timestamps of one dense backward solve (5 per block). */

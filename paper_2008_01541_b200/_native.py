@@ -82,6 +82,7 @@ _SIGS = {
     "spb_last_error": ([], ctypes.c_char_p),
     "spb_device_count": ([P], I32),
     "spb_get_device": ([P], I32),
+    "spb_ctx_cholesky_kind": ([P, P], I32),
     "spb_host_register": ([P, I64], I32),
     "spb_host_unregister": ([P], I32),
     "spb_set_host_blas": ([P, P, P, P, P], I32),

@@ -758,15 +758,11 @@ int Ctx::enqueue_solve(int outer, int inner, int cadence, cudaEvent_t* ev) {
         su = st_aux;
         launches++;
       }
-      // on the main stream the streaming (persistent, TMA-fed) mat-vec; beside
-      // the backward sweep the short-lived per-tile kernel, whose CTAs hold no
-      // shared memory and so leave the sweep's level kernels their SM slots
-      if (overlap) {
-        launch_sym_tile_gemv(su, dd, u2.p, gemv_partial.p);
-        launch_sym_tile_gemv_reduce(su, dd, gemv_partial.p, s0u.p);
-      } else {
-        launch_sym_gemv(su, dd, u2.p, gemv_partial.p, s0u.p, true);
-      }
+      // the streaming (persistent, TMA-fed) mat-vec; beside the backward sweep
+      // on a capped grid, so the sweep's level kernels keep most SM slots
+      // (bitwise the same result either way)
+      static const int aux_ctas = getenv("SPB_GEMV_AUX_CTAS") ? atoi(getenv("SPB_GEMV_AUX_CTAS")) : 48;
+      launch_sym_gemv(su, dd, u2.p, gemv_partial.p, s0u.p, true, overlap ? aux_ctas : 0);
       launch_proxy_wu(su, P_, active.p, u2.p, vprox.p);
       launch_inner_update(su, n2, u2.p, s0u.p, k_ptr.p, k_idx.p, k_val.p, g.p, prox_w.p, vprox.p, gc_ptr.p,
                           gc_src.p, f_tilde2.p, overlap ? nullptr : u2acc.p, x.p, x2_ids.p, r_part.p);
@@ -1045,6 +1041,13 @@ int32_t spb_device_count(int32_t* count) {
     return SPB_ERR_CUDA;
   }
   *count = c;
+  return SPB_OK;
+}
+
+int32_t spb_ctx_cholesky_kind(spb_ctx* cp, int32_t* kind) {
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  if (!c || !kind) { spb::set_error("spb_ctx_cholesky_kind: bad arguments"); return SPB_ERR_ARG; }
+  *kind = c->oz ? 1 : 0;
   return SPB_OK;
 }
 

@@ -2046,7 +2046,8 @@ void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const doubl
 
 // out = sigma0 u: the streaming tile pass, then the fixed-order block sums
 // (both programmatic launches when pdl).
-void launch_sym_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial, double* out, bool pdl) {
+void launch_sym_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial, double* out, bool pdl,
+                     int max_ctas) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sym_gemv_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG_SMEM);
@@ -2057,7 +2058,8 @@ void launch_sym_gemv(cudaStream_t st, const DenseDev& d, const double* u, double
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sym_gemv_stream, SG_THREADS, SG_SMEM);
     per_sm = std::max(1, std::min(per_sm, SG_CTAS_PER_SM));
   }
-  const int grid = std::min(dense_tile_count(d.N), NUM_SMS_B200 * per_sm);
+  int grid = std::min(dense_tile_count(d.N), NUM_SMS_B200 * per_sm);
+  if (max_ctas > 0) grid = std::min(grid, max_ctas);  // results do not depend on the grid
   if (pdl) {
     launch_pdl(k_sym_gemv_stream, dim3(grid), dim3(SG_THREADS), SG_SMEM, st, d, u, partial);
     launch_pdl(k_sym_gemv_reduce4, dim3(d.N), dim3(4 * 3 * TS), 0, st, d, (const double*)partial, out);

@@ -107,7 +107,10 @@ void launch_dense_backward(cudaStream_t st, const DenseDev& d, double* xrows, do
 void dense_backward_preset(cudaStream_t st, const DenseDev& d, double* xrows);  // xrows <- sentinel
 void launch_sym_tile_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial);
 void launch_sym_tile_gemv_reduce(cudaStream_t st, const DenseDev& d, const double* partial, double* out);
-void launch_sym_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial, double* out, bool pdl);
+// max_ctas > 0 caps the persistent grid (beside the backward sweep); the
+// result is bitwise independent of the grid (per-tile partials, fixed-order sums)
+void launch_sym_gemv(cudaStream_t st, const DenseDev& d, const double* u, double* partial, double* out, bool pdl,
+                     int max_ctas = 0);
 
 // -------------------------------------------------------------------- pcg.cu
 struct PcgDev {
