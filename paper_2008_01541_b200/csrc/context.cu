@@ -1615,8 +1615,10 @@ int32_t spb_ctx_trace_cholesky(spb_ctx* cp, uint64_t* out, int32_t* tasks_out, i
   dd.trace = tr;
   SPB_CUDA(cudaMemsetAsync(c->flags.p, 0, sizeof(int) * (spb::dense_tile_count(c->N) + c->N), c->st));
   SPB_CUDA(cudaMemsetAsync(c->counter.p, 0, sizeof(int), c->st));
+  if (getenv("SPB_OZ_DIAG_NOMMA")) spb::chol_int8_diag_nomma(atoi(getenv("SPB_OZ_DIAG_NOMMA")));
   spb::launch_cholesky(c->st, dd, c->tasks.p, c->ntasks, c->chol_grid, false, c->oz);
   SPB_CUDA(cudaStreamSynchronize(c->st));
+  if (getenv("SPB_OZ_DIAG_NOMMA")) spb::chol_int8_diag_nomma(0);
   SPB_CUDA(cudaMemcpy(out, tr, sizeof(unsigned long long) * 4 * c->ntasks, cudaMemcpyDeviceToHost));
   SPB_CUDA(cudaMemcpy(tasks_out, c->tasks.p, sizeof(int2) * c->ntasks, cudaMemcpyDeviceToHost));
   cudaFree(tr);

@@ -1063,7 +1063,9 @@ __device__ __forceinline__ void tile_digits(const double* __restrict__ src, cons
 // One 64-deep k-step of S += L_a L_b^T from their digit planes in smem
 // (sa, sb: 32 KB each; sa == sb for the diagonal tasks). first: the task's
 // first k-step (the first MMA into each TMEM block overwrites).
+__device__ int g_oz_diag_nomma = 0;  // DIAGNOSTIC ONLY (SPB_OZ_DIAG_NOMMA, traced launches): skip the MMAs
 __device__ __forceinline__ void oz_kstep(uint32_t tmem, const signed char* sa, const signed char* sb, bool first) {
+  if (g_oz_diag_nomma) return;
   const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
 #pragma unroll
   for (int h = 0; h < 4; ++h)
@@ -1998,6 +2000,8 @@ void launch_cholesky(cudaStream_t st, const DenseDev& d, const int2* tasks, int 
   }
   k_cholesky_oz<<<grid, NTHREADS, smem, st>>>(d, tasks, ntasks);
 }
+
+void chol_int8_diag_nomma(int on) { cudaMemcpyToSymbol(g_oz_diag_nomma, &on, sizeof(int)); }
 
 bool chol_int8_enabled() {
   static const bool on = !(getenv("SPB_CHOL_INT8") && getenv("SPB_CHOL_INT8")[0] == '0');

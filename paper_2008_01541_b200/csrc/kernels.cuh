@@ -95,6 +95,7 @@ void launch_cholesky_tiles(cudaStream_t st, const DenseDev& d, const int2* tasks
 void launch_cholesky(cudaStream_t st, const DenseDev& d, const int2* tasks, int ntasks, int grid, bool pdl, bool int8);
 // SPB_CHOL_INT8 (default 1): contexts factor with the INT8 tensor-core path
 bool chol_int8_enabled();
+void chol_int8_diag_nomma(int on);  // diagnostics (trace only): skip the INT8 MMAs
 std::vector<int2> cholesky_task_order(int N, bool with_rhs, int lead);
 // P ranks (real: one job per process, P = 1 per launch; emulated: one launch
 // over all ranks' replicas, CTA b serving rank b % P)
