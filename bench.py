@@ -702,6 +702,7 @@ def run_dense(args):
         return
     fp64_peak = measure_fp64_peak()
     top = sweep[-1]
+    int8 = world == 1 and D.DenseCholesky(64, device=0).int8
     line = {
         "metric": "Cholesky FP64 TFLOPS (dense Schur-complement sweep, BASELINE config 4)",
         "value": top["tflops"], "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -712,11 +713,12 @@ def run_dense(args):
                    "parallelism": ("tile-cyclic over %d GPUs (NVLink peer pushes)" % world) if world > 1
                    else "one GPU"},
         "sweep": sweep,
-        "roofline": {"bound": "tensor", "kernel": "k_cholesky_tiles (FP64 DMMA)" if world == 1 else
-                     "k_cholesky_ranks (FP64 DMMA, tile-cyclic)", "achieved": top["tflops"] / world,
-                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": top["tflops"] / world / fp64_peak,
-                     "traffic": None, "flops_per_launch": D.chol_flops(top["m"]),
-                     "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (per GPU)"},
+        "roofline": (cholesky_roofline(True, top["m"], top["ms"], top["tflops"], fp64_peak, None, None) if int8 else
+                     {"bound": "tensor", "kernel": "k_cholesky_tiles (FP64 DMMA)" if world == 1 else
+                      "k_cholesky_ranks (FP64 DMMA, tile-cyclic)", "achieved": top["tflops"] / world,
+                      "peak": fp64_peak, "unit": "TFLOP/s", "frac": top["tflops"] / world / fp64_peak,
+                      "traffic": None, "flops_per_launch": D.chol_flops(top["m"]),
+                      "peak_source": "cuBLAS DGEMM 8192^3 measured live in this run (per GPU)"}),
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -316,6 +316,10 @@ int32_t spb_dense_open_peers(spb_dense *d, const uint8_t *handles /* nranks * SP
  * words) with `value`; peer >= 0 reads the first L value and flag word of the
  * peer's IPC-mapped replica (peer slots in rank order, own rank skipped) */
 int32_t spb_dense_debug_replica(spb_dense *d, int32_t peer, double value, double *out_value, int32_t *out_flag);
+/* 1: one GPU, trailing updates on the INT8 tensor cores (emulated FP64,
+ * k_cholesky_oz); 0: FP64 DMMA (tile-cyclic / emulated ranks, SPB_CHOL_INT8=0) */
+int32_t spb_dense_cholesky_kind(spb_dense *d, int32_t *kind);
+int32_t spb_dense_set_cholesky_kind(spb_dense *d, int32_t kind);
 int32_t spb_dense_reset(spb_dense *d);
 int32_t spb_dense_launch(spb_dense *d);
 int32_t spb_dense_finish(spb_dense *d, double *ms, int64_t *info);

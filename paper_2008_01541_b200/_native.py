@@ -83,6 +83,8 @@ _SIGS = {
     "spb_device_count": ([P], I32),
     "spb_get_device": ([P], I32),
     "spb_ctx_cholesky_kind": ([P, P], I32),
+    "spb_dense_cholesky_kind": ([P, P], I32),
+    "spb_dense_set_cholesky_kind": ([P, I32], I32),
     "spb_host_register": ([P, I64], I32),
     "spb_host_unregister": ([P], I32),
     "spb_set_host_blas": ([P, P, P, P, P], I32),

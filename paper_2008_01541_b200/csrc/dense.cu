@@ -1031,27 +1031,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&u)[32]) {
 
 // digits of a swizzled FP64 tile (rows of block `rb`) into the tile's 8
 // planes in global memory; 4 consecutive columns (one 32-bit word per plane)
-// per work item, threads t0, t0 + nt, ...
+// per work item, threads t0, t0 + nt, ... Each digit is 3 FP64 operations: the
+// magic-number round (t = fma(x, 2^7, 1.5 * 2^52) holds rint(128 x) in its low
+// bits; no float -> int conversion), the exact remainder fma(x, 2^7, -d).
 __device__ __forceinline__ void tile_digits(const double* __restrict__ src, const int* __restrict__ erow, int rb,
                                             signed char* __restrict__ dst, int t0, int nt, int r0, int r1) {
+  constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52
   for (int w = r0 * 16 + t0; w < r1 * 16; w += nt) {
     const int r = w >> 4, c0 = (w & 15) * 4;
-    const double sc = pow2i(-erow[rb * TS + r]);  // exact scaling (no ldexp call)
+    const double sc = pow2i(-erow[rb * TS + r]);  // exact scaling
+    // the 4 logical columns c0 .. c0+3 are 4 adjacent physical ones (swz XORs a multiple of 4)
+    const double2 v01 = *reinterpret_cast<const double2*>(src + swz(r, c0));
+    const double2 v23 = *reinterpret_cast<const double2*>(src + swz(r, c0) + 2);
+    const double xs[4] = {v01.x * sc, v01.y * sc, v23.x * sc, v23.y * sc};
     uint32_t word[NDIG];
 #pragma unroll
     for (int p = 0; p < NDIG; ++p) word[p] = 0u;
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
-      double x = src[swz(r, c0 + cc)] * sc;
-      double dd = rint(x * 64.0);
-      word[0] |= (uint32_t)(uint8_t)(int8_t)dd << (8 * cc);
-      x = x * 64.0 - dd;
+      double x = xs[cc];
 #pragma unroll
-      for (int p = 1; p < NDIG; ++p) {
-        x *= 128.0;
-        dd = rint(x);
-        word[p] |= (uint32_t)(uint8_t)(int8_t)dd << (8 * cc);
-        x -= dd;
+      for (int p = 0; p < NDIG; ++p) {
+        const double m = p == 0 ? 64.0 : 128.0;
+        const double t = fma(x, m, MAGIC);
+        const double dd = t - MAGIC;
+        x = fma(x, m, -dd);
+        word[p] |= ((uint32_t)__double2loint(t) & 0xFFu) << (8 * cc);
       }
     }
     const int off = kmaj_off(r, c0);

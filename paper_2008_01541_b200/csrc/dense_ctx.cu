@@ -164,6 +164,17 @@ __global__ void __launch_bounds__(256) k_tile_matvec(const double* __restrict__ 
     y[b * TS + r] = rowacc + ((colp[0][r] + colp[1][r]) + (colp[2][r] + colp[3][r]));
   }
 }
+// Per-row exponent bounds of the INT8 trailing updates (k_cholesky_oz):
+// 2^erow[r] > sqrt(H_rr) >= |L_rc| (L L^T = H), from the diagonal tiles.
+__global__ void k_erow_from_diag(const double* __restrict__ tiles, int N, int* __restrict__ erow) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= N * TS) return;
+  const int b = r / TS, rr = r % TS;
+  const double h = tiles[(size_t)(b * (b + 1) / 2 + b) * TILE + swz(rr, rr)];
+  int ex = 0;
+  frexp(sqrt(fmax(h, 1e-300)), &ex);
+  erow[r] = ex;
+}
 }  // namespace
 }  // namespace spb
 
@@ -179,6 +190,10 @@ struct spb_dense {
   std::vector<int> ntasks;
   spb::DenseRankJob* jobs = nullptr;  // device copy (MULTI kernel)
   bool jobs_ready = false;
+  // single GPU: trailing updates on the INT8 tensor cores (SPB_CHOL_INT8, default on)
+  bool int8 = false;
+  int* erow = nullptr;
+  signed char* Lq = nullptr;
   cudaStream_t st = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   ~spb_dense() {
@@ -190,6 +205,8 @@ struct spb_dense {
     for (auto* t : tasks) cudaFree(t);
     if (jobs) cudaFree(jobs);
     if (sigma0) cudaFree(sigma0);
+    if (erow) cudaFree(erow);
+    if (Lq) cudaFree(Lq);
     if (e0) cudaEventDestroy(e0);
     if (e1) cudaEventDestroy(e1);
     if (st) cudaStreamDestroy(st);
@@ -332,6 +349,14 @@ int32_t spb_dense_create(int64_t m, int32_t device, int32_t rank, int32_t nranks
   if (emulate || nranks == 1) {
     int s = spb::upload_jobs(d);
     if (s != SPB_OK) return s;
+  }
+  // one GPU: the INT8 tensor-core path needs the per-row bounds and 32 KB of
+  // digit planes per tile (int32 accumulation stays exact up to m ~ 98K:
+  // 4 digit pairs x 64^2 x m < 2^31)
+  d->int8 = !d->multi() && spb::chol_int8_enabled() && m <= 98304;
+  if (d->int8) {
+    SPB_CUDA(cudaMalloc(&d->erow, sizeof(int) * (size_t)d->N * spb::TS));
+    SPB_CUDA(cudaMalloc(&d->Lq, d->ntiles() * (size_t)32768));
   }
   *out = guard.release();
   return SPB_OK;
@@ -483,6 +508,31 @@ int32_t spb_dense_reset(spb_dense* d) {
   SPB_GUARD_END
 }
 
+int32_t spb_dense_set_cholesky_kind(spb_dense* d, int32_t kind) {
+  SPB_GUARD_BEGIN
+  DCHECK(d);
+  if (kind == 1 && (d->multi() || d->m > 98304)) {
+    spb::set_error("spb_dense_set_cholesky_kind: the INT8 path is single-GPU, m <= 98304");
+    return SPB_ERR_ARG;
+  }
+  d->int8 = kind == 1;
+  if (d->int8 && !d->erow) {
+    SPB_CUDA(cudaMalloc(&d->erow, sizeof(int) * (size_t)d->N * spb::TS));
+    SPB_CUDA(cudaMalloc(&d->Lq, d->ntiles() * (size_t)32768));
+  }
+  return SPB_OK;
+  SPB_GUARD_END
+}
+
+int32_t spb_dense_cholesky_kind(spb_dense* d, int32_t* kind) {
+  if (!d || !kind) {
+    spb::set_error("spb_dense_cholesky_kind: bad arguments");
+    return SPB_ERR_ARG;
+  }
+  *kind = d->int8 ? 1 : 0;
+  return SPB_OK;
+}
+
 int32_t spb_dense_launch(spb_dense* d) {
   SPB_GUARD_BEGIN
   DCHECK(d);
@@ -502,7 +552,12 @@ int32_t spb_dense_launch(spb_dense* d) {
     dd.flags = r.flags(d->lo);
     dd.counter = r.counter(d->lo);
     dd.info = r.info(d->lo);
-    spb::launch_cholesky_tiles(d->st, dd, d->tasks[0], d->ntasks[0], d->grid);
+    if (d->int8) {
+      spb::k_erow_from_diag<<<(d->N * spb::TS + 255) / 256, 256, 0, d->st>>>(d->sigma0, d->N, d->erow);
+      dd.erow = d->erow;
+      dd.Lq = d->Lq;
+    }
+    spb::launch_cholesky(d->st, dd, d->tasks[0], d->ntasks[0], d->grid, false, d->int8);
   } else {
     spb::launch_cholesky_ranks(d->st, d->jobs, (int)d->reps.size(), d->grid);
   }

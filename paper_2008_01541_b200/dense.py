@@ -67,7 +67,8 @@ def tile_owner(i: int, j: int, nranks: int) -> int:
 class DenseCholesky:
     """One dense SPD matrix on the device and its tile Cholesky factor."""
 
-    def __init__(self, m: int, device: int = 0, rank: int = 0, nranks: int = 1, emulate: bool = False):
+    def __init__(self, m: int, device: int = 0, rank: int = 0, nranks: int = 1, emulate: bool = False,
+                 int8: Optional[bool] = None):
         if m <= 0:
             raise InvalidArgumentError("order must be positive")
         if not (1 <= nranks <= MAX_RANKS):
@@ -78,6 +79,8 @@ class DenseCholesky:
         nat.check(nat.lib().spb_dense_create(self.m, device, self.rank, self.nranks, int(self.emulate),
                                             ctypes.byref(h)))
         self._h = h
+        if int8 is not None:  # default: INT8 tensor cores on one GPU (SPB_CHOL_INT8), DMMA otherwise
+            nat.check(nat.lib().spb_dense_set_cholesky_kind(self._h, 1 if int8 else 0))
 
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
@@ -93,6 +96,14 @@ class DenseCholesky:
     @property
     def replicas(self) -> int:
         return self.nranks if self.emulate else 1
+
+    @property
+    def int8(self) -> bool:
+        """True when the trailing updates run on the INT8 tensor cores
+        (emulated FP64, one GPU); False: FP64 DMMA (tile-cyclic ranks)."""
+        k = ctypes.c_int32(0)
+        nat.check(nat.lib().spb_dense_cholesky_kind(self._h, ctypes.byref(k)))
+        return bool(k.value)
 
     # -------------------------------------------------------------- matrix
     def set_matrix(self, h: np.ndarray) -> None:

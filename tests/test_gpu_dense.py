@@ -83,7 +83,7 @@ def test_emulated_tile_cyclic_replicas_bit_identical(P):
     from paper_2008_01541_b200.dense import DenseCholesky
 
     m = 1000 if P != 8 else 2100
-    one = DenseCholesky(m)
+    one = DenseCholesky(m, int8=False)  # the tile-cyclic ranks run the FP64 DMMA kernel
     one.synthetic()
     one.factor()
     ref = one.factor_lower()
@@ -119,3 +119,23 @@ def test_full_size_residual(m):
     d.factor()
     rr, aa = d.residual(np.random.default_rng(m).standard_normal(m))
     assert rr <= 1e-13 * aa
+
+
+@pytest.mark.parametrize("m", [700, 3000, 6197])
+def test_int8_tensor_core_factor_matches_fp64(m):
+    """The emulated-FP64 factor (INT8 tcgen05 trailing updates, 8 digit
+    planes) against the FP64 DMMA factor of the same matrix: 1e-13 of max|L|,
+    and the residual ||A v - L L^T v|| / ||A v|| at the FP64 level."""
+    from paper_2008_01541_b200.dense import DenseCholesky
+
+    a = DenseCholesky(m, int8=True)
+    b = DenseCholesky(m, int8=False)
+    assert a.int8 and not b.int8
+    for d in (a, b):
+        d.synthetic()
+        d.factor()
+    La, Lb = a.factor_lower(), b.factor_lower()
+    assert np.abs(La - Lb).max() <= 1e-13 * np.abs(Lb).max()
+    v = np.random.default_rng(m).standard_normal(m)
+    rr, aa = a.residual(v)
+    assert rr <= 1e-14 * aa * 10
