@@ -202,6 +202,14 @@ int32_t spb_ctx_step(spb_ctx *ctx, const spb_step_config *cfg, spb_frame_metrics
 int32_t spb_ctx_frame(spb_ctx *ctx, const double *att_targets, int32_t num_colliders,
                       const spb_posed_collider *colliders, double *x, uint8_t *active, double *target,
                       const spb_step_config *cfg, double *f_tilde2, double *u2_accum, spb_frame_metrics *metrics);
+/* spb_ctx_frame with the incoming active set / targets read from *_in and the
+ * outgoing ones written to active / target (a caller that keeps the previous
+ * frame's arrays, as SolverState does, passes them as *_in and fresh arrays
+ * as outputs; no copy on the host). */
+int32_t spb_ctx_frame_io(spb_ctx *ctx, const double *att_targets, int32_t num_colliders,
+                         const spb_posed_collider *colliders, double *x, const uint8_t *active_in,
+                         const double *target_in, uint8_t *active, double *target, const spb_step_config *cfg,
+                         double *f_tilde2, double *u2_accum, spb_frame_metrics *metrics);
 /* PCG baseline (reference solve_frame_pcg, solver.py:542-603; the paper's
  * §5.4 comparison solver), on the device. spb_ctx_set_operator hands over the
  * global matrix A (reference GlobalSystem.A: upper CSC in partition order,

@@ -105,6 +105,7 @@ _SIGS = {
     "spb_ctx_set_state": ([P, P, P, P, P, P, P, P], I32),
     "spb_ctx_step": ([P, P, P], I32),
     "spb_ctx_frame": ([P, P, I32, P, P, P, P, P, P, P, P], I32),
+    "spb_ctx_frame_io": ([P, P, I32, P, P, P, P, P, P, P, P, P, P], I32),
     "spb_ctx_get_state": ([P, P, P, P, P, P, P, P], I32),
     "spb_ctx_bench": ([P, P, I32, P, P], I32),
     "spb_ctx_bench_cholesky": ([P, I32, P], I32),

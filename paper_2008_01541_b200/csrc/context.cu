@@ -1359,6 +1359,13 @@ int32_t spb_ctx_step(spb_ctx* cp, const spb_step_config* cfg, spb_frame_metrics*
 int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
                       double* x, uint8_t* active, double* target, const spb_step_config* cfg, double* f_tilde2,
                       double* u2_accum, spb_frame_metrics* m) {
+  return spb_ctx_frame_io(cp, att_targets, ncol, cols, x, active, target, active, target, cfg, f_tilde2, u2_accum, m);
+}
+
+int32_t spb_ctx_frame_io(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
+                         double* x, const uint8_t* active_in, const double* target_in, uint8_t* active,
+                         double* target, const spb_step_config* cfg, double* f_tilde2, double* u2_accum,
+                         spb_frame_metrics* m) {
   SPB_GUARD_BEGIN
   Ctx* c = reinterpret_cast<Ctx*>(cp);
   SPB_CUDA(cudaSetDevice(c->device));
@@ -1392,14 +1399,15 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
     memcpy(c->cols_host->posed[i].t, cols[i].translation, sizeof(double) * 3);
   }
   if (c->P) {
-    memcpy(hs + c->off_act, active, c->P);
-    memcpy(hs + c->off_tgt, target, sizeof(double) * 3 * c->P);
+    memcpy(hs + c->off_act, active_in, c->P);
+    memcpy(hs + c->off_tgt, target_in, sizeof(double) * 3 * c->P);
   }
   TRY(c->sync_shapes());
   const size_t up_bytes = c->P ? c->off_tgt + sizeof(double) * 3 * c->P : c->off_act;
   SPB_CUDA(cudaMemcpyAsync(c->io_dev, hs, up_bytes, cudaMemcpyHostToDevice, c->st));
+  const size_t xbytes = sizeof(double) * 3 * c->n;
   IoList up;
-  up.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  up.add(c->x.p, x, xbytes);
   TRY(io_upload(c, up, false));
   if (io_trace) {
     cudaEventRecord(tev[1], c->st);
@@ -1416,7 +1424,7 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
   SPB_CUDA(cudaMemcpyAsync(hs + c->off_act, c->io_dev + c->off_act, c->off_end - c->off_act,
                            cudaMemcpyDeviceToHost, c->st));
   IoList down;
-  down.add(c->x.p, x, sizeof(double) * 3 * c->n);
+  down.add(c->x.p, x, xbytes);
   TRY(io_download(c, down, c->st_io, true));  // synchronises both streams
   if (c->P) {
     memcpy(active, hs + c->off_act, c->P);
