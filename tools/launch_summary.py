@@ -18,7 +18,7 @@ for r in rows:
 names = [d["Kernel Name"] for d in data]
 idx = [i for i, n in enumerate(names) if "k_finish_metrics" in n]
 bounds = [(idx[k - 1] + 1 if k else 0, idx[k] + 1) for k in range(len(idx))] or [(0, len(data))]
-schur = [b for b in bounds if sum("k_cholesky_tiles" in names[i] for i in range(*b)) == 1]
+schur = [b for b in bounds if sum("k_cholesky" in names[i] for i in range(*b)) == 1]
 start, end = (schur or bounds)[-1]
 tot, cnt, seq = collections.defaultdict(float), collections.Counter(), []
 for d in data[start:end]:
