@@ -38,6 +38,12 @@ constexpr int NUM_SMS_B200 = 148;
 // every 64th spin, so a flag that is already set costs nothing extra.
 constexpr unsigned long long kSpinLimitNs = 60ull * 1000ull * 1000ull * 1000ull;  // 60 s
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct SpinGuard {
   unsigned long long t0 = 0;
   unsigned it = 0;

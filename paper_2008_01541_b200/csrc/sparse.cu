@@ -1444,6 +1444,16 @@ void sweep_work_free(SweepWork& w) {
   w = SweepWork{};
 }
 
+// DIAGNOSTIC ONLY (tools/sweep_levels.sh): skip the launches of the upper
+// levels in the SPB_SWEEP_SKIP bitmask (level kernels and gathers) or of the
+// gathers in SPB_SWEEP_SKIPG; the results are then wrong, the timing tells
+// each level's marginal cost in the PDL-chained sweep
+static long sweep_skip(bool gather) {
+  static const long m = getenv("SPB_SWEEP_SKIP") ? strtol(getenv("SPB_SWEEP_SKIP"), nullptr, 0) : 0;
+  static const long g = getenv("SPB_SWEEP_SKIPG") ? strtol(getenv("SPB_SWEEP_SKIPG"), nullptr, 0) : 0;
+  return gather ? (m | g) : m;
+}
+
 void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, double* y, double* U, double* f2,
                     int* launches, const SweepWork* w) {
   double* VZ = w ? w->VZ : d.VZ;
@@ -1463,7 +1473,8 @@ void sparse_forward(cudaStream_t st, const DeviceFactor& d, const double* b, dou
   }
   for (int l = d.fuse; l < d.nlevels && !d.flow; ++l) {
     const LevelTasks& T = d.lv[l];
-    if (T.npos == 0) continue;
+    if (T.npos == 0 || ((sweep_skip(false) >> l) & 1)) continue;
+    if (!((sweep_skip(true) >> l) & 1))
     launch_pdl(k_fw_gather, dim3(ceil_div(T.npos, 256)), dim3(256), 0, st, (const int*)(d.lvl_pos + T.pos_off),
                T.npos, (const int*)d.pos_owner, (const int*)d.asm_ptr, (const int*)d.asm_src, (const double*)U, b,
                VZ);
@@ -1501,7 +1512,7 @@ void sparse_backward(cudaStream_t st, const DeviceFactor& d, const double* y, do
     if (T.npos == 0) continue;
     const int nt = d.bwt_off[l + 1] - d.bwt_off[l];
     const int nw = d.bww_off[l + 1] - d.bww_off[l];
-    if (nt + nw == 0) continue;
+    if (nt + nw == 0 || ((sweep_skip(false) >> l) & 1)) continue;
     if (nt)
       launch_pdl(k_bw_level, dim3(nt), dim3(256), sizeof(double) * 3 * T.bw_rows, st, (const SnDev*)d.sn,
                  (const double*)d.M, (const int4*)(d.bw_tiles + d.bwt_off[l]), T.bw_rows,
