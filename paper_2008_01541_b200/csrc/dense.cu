@@ -443,8 +443,18 @@ __device__ __forceinline__ void potrf_diag16(double* S, double* DT, int o, int j
 __device__ long long g_potrf_prof[32];
 #define POTRF_MARK(n) \
   if (threadIdx.x == 0) g_potrf_prof[n] += clock64();
+#define POTRF_MARKW(n) \
+  if (threadIdx.x == SPB_POTRF_PROF_T) g_potrf_prof[16 + (n)] += clock64();
+#define POTRF_MARK0(n) \
+  if (threadIdx.x == 0) g_potrf_prof[n] += clock64();
 #else
 #define POTRF_MARK(n)
+#define POTRF_MARKW(n) \
+  do {                 \
+  } while (0);
+#define POTRF_MARK0(n) \
+  do {                 \
+  } while (0);
 #endif
 
 // rank-16 update of the 8x8 block (rb, cb) of the augmented panel by the
@@ -641,8 +651,11 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
           upd_block2_tile(S, upd, rbu[0], cbu[0], oku[0], rbu[1], cbu[1], oku[1], g, t);
         }
       }
+      if (kb == 1) POTRF_MARKW(0)
       if (kb < 3) init_rows(o + 16, tid - 32, NCONS - 32);
+      if (kb == 1) POTRF_MARKW(1)
       if (kb > 0) store_cols(o - 16, tid - 32, NCONS - 32, true, true);
+      if (kb == 1) POTRF_MARKW(2)
     }
     if (warp > 0 && kb > 0) {
       // only the 8x8 blocks the update changes, listed compactly: the lower
@@ -678,6 +691,8 @@ __device__ void potrf_blocked_tile(const Acc& acc, double* S, double* DT, double
         upd_block2(S, o - 16, rbu[0], cbu[0], oku[0], rbu[1], cbu[1], oku[1], g, t);
       }
     }
+    if (kb == 1) POTRF_MARKW(3)
+    if (kb == 1) POTRF_MARK0(24)  // warp 0 done (block 1)
     cons_sync();
     POTRF_MARK(2 + 2 * kb)
     // (b) panel: rows [o+16, 128) x cols [o, o+16): P = S_panel * D^-T (in place)

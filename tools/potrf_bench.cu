@@ -2,6 +2,9 @@
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2008_01541_b200/csrc potrf_bench.cu ...
 #ifndef NOPROF
 #define SPB_POTRF_PROF 1
+#ifndef SPB_POTRF_PROF_T
+#define SPB_POTRF_PROF_T 32
+#endif
 #endif
 #include "../paper_2008_01541_b200/csrc/dense.cu"
 
@@ -78,6 +81,10 @@ int main() {
     prev = prof[k];
   }
   printf("  %-10s %8.0f cyc\n", "store", (prof[14] - prev) / 20.0);
+  // block 1, the profiled thread of warps 1-7 (from the block's start = mark 3 of block 0)
+  printf("  block 1 thread %d: +%.0f to its branch, init_rows %.0f, store_cols %.0f, trailing update %.0f (warp 0 done at +%.0f; barrier at +%.0f)\n",
+         SPB_POTRF_PROF_T, (prof[16] - prof[3]) / 20.0, (prof[17] - prof[16]) / 20.0, (prof[18] - prof[17]) / 20.0,
+         (prof[19] - prof[18]) / 20.0, (prof[24] - prof[3]) / 20.0, (prof[4] - prof[3]) / 20.0);
 #endif
   double hL[4096];
   cudaMemcpy(hL, L, 4096 * 8, cudaMemcpyDeviceToHost);
