@@ -14,7 +14,7 @@ void set_error(const std::string&) {}
 using namespace spb;
 
 __global__ void __launch_bounds__(288, 1) k_potrf_bench(const double* A, double* L, double* LiT, int* info,
-                                                       long long* cycles, int reps) {
+                                                       long long* cycles, int reps, const double* U) {
   extern __shared__ __align__(128) double smd[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (warp == 8) return;  // consumers only (named barrier 1 counts 256)
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(288, 1) k_potrf_bench(const double* A, double*
   long long t0 = clock64();
   const DensePeers nop{};
   for (int r = 0; r < reps; ++r)
-    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop, nullptr);
+    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop, U);
   long long t1 = clock64();
   // diag16 alone
   for (int r = 0; r < reps; ++r) {
@@ -60,7 +60,16 @@ int main() {
   cudaMemcpy(A, hA, 4096 * 8, cudaMemcpyHostToDevice);
   size_t smem = cholesky_smem_bytes();
   cudaFuncSetAttribute(k_potrf_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_potrf_bench<<<1, 288, smem>>>(A, L, LiT, info, cyc, 20);
+  // U (swizzled 64 x 64, the diagonal task's sub-diagonal tile): its rank-64
+  // update A - U U^T runs in block 0 (POTRF_UPD=1) or is skipped
+  double hU[4096];
+  const bool with_u = getenv("POTRF_UPD") && getenv("POTRF_UPD")[0] == '1';
+  for (int r = 0; r < 64; ++r)
+    for (int c = 0; c < 64; ++c) hU[swz(r, c)] = 0.05 * ((r * 7 + c * 13) % 11 - 5) / 5.0;
+  double* U;
+  cudaMalloc(&U, 4096 * 8);
+  cudaMemcpy(U, hU, 4096 * 8, cudaMemcpyHostToDevice);
+  k_potrf_bench<<<1, 288, smem>>>(A, L, LiT, info, cyc, 20, with_u ? U : nullptr);
   cudaDeviceSynchronize();
   long long h[3];
   cudaMemcpy(h, cyc, 24, cudaMemcpyDeviceToHost);
@@ -88,14 +97,27 @@ int main() {
 #endif
   double hL[4096];
   cudaMemcpy(hL, L, 4096 * 8, cudaMemcpyDeviceToHost);
-  // check L L^T == A
+  // check L L^T == A - U U^T
   double err = 0;
   for (int r = 0; r < 64; ++r)
     for (int c = 0; c <= r; ++c) {
       double s = 0;
       for (int k = 0; k <= c; ++k) s += hL[swz(r, k)] * hL[swz(c, k)];
-      err = fmax(err, fabs(s - hA[r * 64 + c]));
+      double a = hA[r * 64 + c];
+      if (with_u)
+        for (int k = 0; k < 64; ++k) a -= hU[swz(r, k)] * hU[swz(c, k)];
+      err = fmax(err, fabs(s - a));
     }
+  // and L^-T: L^T (L^-T) = I
+  double hLi[4096], erri = 0;
+  cudaMemcpy(hLi, LiT, 4096 * 8, cudaMemcpyDeviceToHost);
+  for (int r = 0; r < 64; ++r)
+    for (int c = 0; c < 64; ++c) {
+      double s = 0;
+      for (int k = 0; k < 64; ++k) s += hL[swz(k, r)] * hLi[swz(k, c)];
+      erri = fmax(erri, fabs(s - (r == c ? 1.0 : 0.0)));
+    }
+  printf("max |L^T L^-T - I| = %.3e\n", erri);
   printf("max |LL^T - A| = %.3e\n", err);
   return 0;
 }
