@@ -45,6 +45,7 @@ def main():
         t = got.get("dram__bytes_read.sum", 0) + got.get("dram__bytes_write.sum", 0)
         js = {"kernel": name.split("(")[0], "traffic_bytes": t, "duration_s": got.get("gpu__time_duration.sum"),
               "dram_read_bytes": got.get("dram__bytes_read.sum"), "dram_write_bytes": got.get("dram__bytes_write.sum"),
+              "l2_hit_pct": got.get("lts__t_sector_hit_rate.pct"),
               "dmma_active_pct": got.get(
                   "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
               "source": rep}
