@@ -499,6 +499,8 @@ def run_b200(args):
         line["inner5"] = {"outer_iters": args.outer, "inner_iters": 5, "ms_per_frame": ms5.value,
                           "frames_per_s": 1e3 / ms5.value,
                           "note": "device-resident, measured after the headline frames on the same context"}
+    if world == 1 and sim.partition.n2 > 0:
+        line["cholesky_accuracy"] = cholesky_accuracy(sim)
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sec, times = cpu_oracle_frames(sim, args.cpu_frames, threads)
@@ -508,6 +510,40 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def cholesky_accuracy(sim):
+    """The timed factorization computes in emulated FP64 (INT8 digit planes,
+    §4.0 of DESIGN.md): the scene's largest H = Σ₀ + C22 (every proxy
+    active) factored by the product path (INT8), by the FP64 DMMA kernel and
+    by LAPACK dpotrf (numpy), outside every timed region. Reports the max
+    entry error of each device factor relative to max |L_LAPACK|, and the
+    INT8 solve residual."""
+    import numpy as np
+
+    import paper_2008_01541_b200 as P
+    from paper_2008_01541_b200 import collision as col
+    from paper_2008_01541_b200 import dense as pdense
+
+    np_ = len(sim.model.proxies)
+    act = col.ActiveSet(np.ones(np_, dtype=bool), np.zeros((np_, 3)))
+    h = np.asarray(sim.system.factor.sigma0) + col.assemble_c22(sim.model.proxies, act, sim.partition,
+                                                               sim.mesh).full().toarray()
+    ref = np.linalg.cholesky(h)
+    scale = np.abs(ref).max()
+    out = {"matrix": f"H = sigma0 + C22, all {np_} proxies active (m = {h.shape[0]})"}
+    for name, int8 in (("int8_emulated", True), ("fp64_dmma", False)):
+        d = pdense.DenseCholesky(h.shape[0], int8=int8)
+        d.set_matrix(h)
+        d.factor()
+        out[f"{name}_vs_lapack_max_rel"] = float(np.abs(d.factor_lower() - ref).max() / scale)
+        d.close()
+    f = P.dense_factor(h)
+    g = np.random.default_rng(5).normal(size=(h.shape[0], 3))
+    u = P.dense_solve(f, g)
+    out["int8_solve_rel_residual"] = float(np.linalg.norm(h @ u - g) / np.linalg.norm(g))
+    out["bar"] = "tests/test_gpu_fullsize.py: factor 1e-12 of max|L|, solve residual 1e-10"
+    return out
 
 
 def pcg_baseline(sim, args, frames: int = 3):
