@@ -24,10 +24,17 @@ __global__ void __launch_bounds__(288, 1) k_potrf_bench(const double* A, double*
     acc.c[mb][nb][0] = A[r * 64 + c];
     acc.c[mb][nb][1] = A[r * 64 + c + 1];
   });
+  // the sub-diagonal tile sits in the shared scratch tile in the kernel
+  double* Us = nullptr;
+  if (U) {
+    Us = smd + SM_SCR;
+    for (int q = tid; q < TILE; q += 256) Us[q] = U[q];
+  }
+  cons_sync();
   long long t0 = clock64();
   const DensePeers nop{};
   for (int r = 0; r < reps; ++r)
-    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop, U);
+    potrf_blocked_tile<false>(acc, smd, smd + 128 * LSP, L, LiT, 0, info, nullptr, wr, wc, lane, nop, Us);
   long long t1 = clock64();
   // diag16 alone
   for (int r = 0; r < reps; ++r) {
