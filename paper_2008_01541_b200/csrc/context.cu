@@ -1362,30 +1362,19 @@ int32_t spb_ctx_frame(spb_ctx* cp, const double* att_targets, int32_t ncol, cons
   return spb_ctx_frame_io(cp, att_targets, ncol, cols, x, active, target, active, target, cfg, f_tilde2, u2_accum, m);
 }
 
-int32_t spb_ctx_frame_io(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
-                         double* x, const uint8_t* active_in, const double* target_in, uint8_t* active,
-                         double* target, const spb_step_config* cfg, double* f_tilde2, double* u2_accum,
-                         spb_frame_metrics* m) {
-  SPB_GUARD_BEGIN
-  Ctx* c = reinterpret_cast<Ctx*>(cp);
-  SPB_CUDA(cudaSetDevice(c->device));
-  auto t0 = std::chrono::steady_clock::now();
-  memset(m, 0, sizeof(*m));
+// The packed-IO frame in two halves, so a batch of contexts can have every
+// frame in flight before the host waits on any (spb_frame_batch):
+// frame_io_enqueue packs the small inputs (pose, active, target) into the
+// pinned small-IO block (ONE copy), uploads x (DMA when the caller
+// page-locked it), launches the frame and enqueues the downloads (x on the io
+// stream from the in-graph "state final" event, overlapping the metrics
+// kernels; [active .. info] in one copy behind the metrics);
+// frame_io_finish waits and unpacks.
+static int frame_io_enqueue(Ctx* c, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
+                            double* x, const uint8_t* active_in, const double* target_in,
+                            const spb_step_config* cfg, IoList& down, IoPending& pend) {
   if (ncol > spb::MAX_COLLIDERS) { spb::set_error("too many colliders"); return SPB_ERR_ARG; }
   SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
-  // SPB_IO_TRACE=1: device-side spans of the call (upload, frame, download)
-  static const bool io_trace = getenv("SPB_IO_TRACE") && getenv("SPB_IO_TRACE")[0] == '1';
-  cudaEvent_t tev[4] = {};
-  auto host_ms = [&]() { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
-  double th[4] = {};
-  if (io_trace) {
-    for (auto& e : tev) cudaEventCreate(&e);
-    cudaEventRecord(tev[0], c->st);
-    th[0] = host_ms();
-  }
-  // ---- inputs: x by DMA (page-locked by the caller) or staged; everything
-  // else (pose, active, target) packed into the pinned small-IO block and
-  // moved by ONE copy
   char* hs = c->io_small_host;
   if (c->na > 0 && att_targets) memcpy(hs + c->off_att, att_targets, sizeof(double) * 3 * c->na);
   c->cols_host->n = ncol;
@@ -1409,23 +1398,16 @@ int32_t spb_ctx_frame_io(spb_ctx* cp, const double* att_targets, int32_t ncol, c
   IoList up;
   up.add(c->x.p, x, xbytes);
   TRY(io_upload(c, up, false));
-  if (io_trace) {
-    cudaEventRecord(tev[1], c->st);
-    th[1] = host_ms();
-  }
   TRY(frame_enqueue(c, cfg, nullptr, true));
-  if (io_trace) {
-    cudaEventRecord(tev[2], c->st);
-    th[2] = host_ms();
-  }
-  // ---- outputs: x on the io stream from the in-graph "state final" event,
-  // overlapping the metrics kernels; [active .. info] (active, target, f~2,
-  // u2_accum, metrics, info) in one copy behind the metrics
   SPB_CUDA(cudaMemcpyAsync(hs + c->off_act, c->io_dev + c->off_act, c->off_end - c->off_act,
                            cudaMemcpyDeviceToHost, c->st));
-  IoList down;
   down.add(c->x.p, x, xbytes);
-  TRY(io_download(c, down, c->st_io, true));  // synchronises both streams
+  return io_download_enqueue(c, down, c->st_io, true, pend);
+}
+static int frame_io_finish(Ctx* c, const IoList& down, const IoPending& pend, uint8_t* active, double* target,
+                           double* f_tilde2, double* u2_accum) {
+  TRY(io_download_finish(c, down, c->st_io, pend));  // synchronises both streams
+  const char* hs = c->io_small_host;
   if (c->P) {
     memcpy(active, hs + c->off_act, c->P);
     memcpy(target, hs + c->off_tgt, sizeof(double) * 3 * c->P);
@@ -1435,16 +1417,39 @@ int32_t spb_ctx_frame_io(spb_ctx* cp, const double* att_targets, int32_t ncol, c
     if (u2_accum) memcpy(u2_accum, hs + c->off_u2, sizeof(double) * 3 * c->n2);
   }
   if (c->n2 == 0) *reinterpret_cast<int*>(c->metrics_host + 4) = 0;
+  return SPB_OK;
+}
+
+int32_t spb_ctx_frame_io(spb_ctx* cp, const double* att_targets, int32_t ncol, const spb_posed_collider* cols,
+                         double* x, const uint8_t* active_in, const double* target_in, uint8_t* active,
+                         double* target, const spb_step_config* cfg, double* f_tilde2, double* u2_accum,
+                         spb_frame_metrics* m) {
+  SPB_GUARD_BEGIN
+  Ctx* c = reinterpret_cast<Ctx*>(cp);
+  SPB_CUDA(cudaSetDevice(c->device));
+  auto t0 = std::chrono::steady_clock::now();
+  memset(m, 0, sizeof(*m));
+  // SPB_IO_TRACE=1: device-side spans of the call (upload + frame, download)
+  static const bool io_trace = getenv("SPB_IO_TRACE") && getenv("SPB_IO_TRACE")[0] == '1';
+  cudaEvent_t tev[3] = {};
   if (io_trace) {
-    th[3] = host_ms();
-    cudaEventRecord(tev[3], c->st_io);
-    cudaEventSynchronize(tev[3]);
-    float a = 0, b = 0, d = 0;
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], c->st);
+  }
+  IoList down;
+  IoPending pend;
+  TRY(frame_io_enqueue(c, att_targets, ncol, cols, x, active_in, target_in, cfg, down, pend));
+  if (io_trace) cudaEventRecord(tev[1], c->st);
+  const double t_issued = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  TRY(frame_io_finish(c, down, pend, active, target, f_tilde2, u2_accum));
+  if (io_trace) {
+    cudaEventRecord(tev[2], c->st_io);
+    cudaEventSynchronize(tev[2]);
+    float a = 0, b = 0;
     cudaEventElapsedTime(&a, tev[0], tev[1]);
     cudaEventElapsedTime(&b, tev[1], tev[2]);
-    cudaEventElapsedTime(&d, tev[2], tev[3]);
-    fprintf(stderr, "[io] gpu: upload %.3f frame %.3f download %.3f ms | host: enter->upload-issued %.3f "
-            "->frame-issued %.3f ->synced %.3f ms\n", a, b, d, th[1], th[2], th[3]);
+    fprintf(stderr, "[io] gpu: upload+frame+state %.3f, tail %.3f ms | host: issued %.3f, done %.3f ms\n", a, b,
+            t_issued, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     for (auto& e : tev) cudaEventDestroy(e);
   }
   m->t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -1468,27 +1473,16 @@ int32_t spb_frame_batch(spb_ctx** ctxs, int32_t n, const spb_frame_io* io, const
     const spb_frame_io& f = io[k];
     memset(&metrics[k], 0, sizeof(spb_frame_metrics));
     SPB_CUDA(cudaSetDevice(c->device));
-    SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
-    TRY(pose_upload(c, f.att_targets, f.num_colliders, f.colliders));
-    IoList up;
-    up.add(c->x.p, f.x, sizeof(double) * 3 * c->n);
-    if (c->P) up.add(c->active.p, f.active, c->P);
-    if (c->P) up.add(c->target.p, f.target, sizeof(double) * 3 * c->P);
-    TRY(io_upload(c, up, false));
-    TRY(frame_enqueue(c, cfg, nullptr));
-    IoList& down = downs[k];
-    down.add(c->x.p, f.x, sizeof(double) * 3 * c->n);
-    if (c->P) down.add(c->active.p, f.active, c->P);
-    if (c->P) down.add(c->target.p, f.target, sizeof(double) * 3 * c->P);
-    if (c->n2) down.add(c->f_tilde2.p, f.f_tilde2, sizeof(double) * 3 * c->n2);
-    if (c->n2) down.add(c->u2acc.p, f.u2_accum, sizeof(double) * 3 * c->n2);
-    TRY(io_download_enqueue(c, down, c->st_io, true, pend[k]));
+    // the packed-IO path of spb_ctx_frame_io (active / target in place)
+    TRY(frame_io_enqueue(c, f.att_targets, f.num_colliders, f.colliders, f.x, f.active, f.target, cfg, downs[k],
+                         pend[k]));
   }
   int rc = SPB_OK;
   for (int k = 0; k < n; ++k) {
     Ctx* c = reinterpret_cast<Ctx*>(ctxs[k]);
+    const spb_frame_io& f = io[k];
     SPB_CUDA(cudaSetDevice(c->device));
-    TRY(io_download_finish(c, downs[k], c->st_io, pend[k]));
+    TRY(frame_io_finish(c, downs[k], pend[k], f.active, f.target, f.f_tilde2, f.u2_accum));
     metrics[k].t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     const int r = frame_finish(c, &metrics[k]);
     if (r != SPB_OK && rc == SPB_OK) rc = r;
