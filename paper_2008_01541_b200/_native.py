@@ -464,10 +464,10 @@ def posed(shape_id: int, rotation, translation) -> PosedCollider:
     p = PosedCollider()
     p.shape = shape_id
     r = f64(rotation).ravel(); t = f64(translation).ravel()
-    for k in range(9):
-        p.rotation[k] = float(r[k])
-    for k in range(3):
-        p.translation[k] = float(t[k])
+    if r.size != 9 or t.size != 3:
+        raise ValueError("collider rotation must be 3 x 3 and translation 3-vector")
+    ctypes.memmove(p.rotation, r.ctypes.data, 72)
+    ctypes.memmove(p.translation, t.ctypes.data, 24)
     return p
 
 
