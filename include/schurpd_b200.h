@@ -286,6 +286,16 @@ int32_t spb_op_elastic(int64_t ne, const int64_t *tets, const double *dm_inverse
 int32_t spb_op_detect(int64_t n, const double *x, const int64_t *tets, int64_t P, const int64_t *proxy_elements,
                       const double *proxy_weights, int32_t num_shapes, const spb_shape_desc *shapes,
                       const spb_posed_collider *colliders, uint8_t *active, double *target, double *depth);
+/* collision.scatter_proxies (reference collision.py:255-300) on the device,
+ * the proxies of every surface triangle (ns x 3) whose three
+ * vertices have node_mask set, per_element each at the given barycentric
+ * points (per_element x 3), owned by the first tet (element order) with that
+ * face; out_elem[ns * per_element], out_weights[ns * per_element * 4];
+ * *count = proxies written (surface-triangle order, then point order).
+ * SPB_ERR_ARG: node ids >= 2^21 or a selected triangle that is no tet's face. */
+int32_t spb_scatter_proxies(const int64_t *tets, int64_t ne, int64_t n, const int64_t *surface_tris, int64_t ns,
+                            const uint8_t *node_mask, int32_t per_element, const double *bary, int64_t *out_elem,
+                            double *out_weights, int64_t *count);
 /* dense SPD factor (lower, in place on a row-major m x m copy) and solve with nrhs columns */
 int32_t spb_op_dense_factor(int64_t m, const double *h, double *chol, int64_t *info);
 int32_t spb_op_dense_solve(int64_t m, const double *chol, int64_t nrhs, const double *g, double *x);

@@ -119,6 +119,7 @@ _SIGS = {
     "spb_op_svd": ([I64, P, P, P, P, P, P, F64, F64], I32),
     "spb_op_elastic": ([I64, P, P, P, I64, P, P, P, F64, F64, I64, P, P, P], I32),
     "spb_op_detect": ([I64, P, P, I64, P, P, I32, P, P, P, P, P], I32),
+    "spb_scatter_proxies": ([P, I64, I64, P, I64, P, I32, P, P, P, P], I32),
     "spb_op_dense_factor": ([I64, P, P, P], I32),
     "spb_op_dense_solve": ([I64, P, I64, P, P], I32),
     "spb_op_forward_sub": ([P, I64, P, P, P, P], I32),
@@ -458,6 +459,30 @@ def shape_desc(shape) -> ShapeDesc:
         d.params[k] = float(prm[k])
     d._keep = keep
     return d
+
+
+def scatter_proxies(tets: np.ndarray, n: int, surface_tris: np.ndarray, mask: np.ndarray, per_element: int,
+                    bary: np.ndarray):
+    """collision.scatter_proxies on the device (spb_scatter_proxies): (elements,
+    weights) of the proxies, or None when the device path does not apply
+    (no GPU, node ids >= 2^21, a triangle that is no tet's face)."""
+    if os.environ.get("SPB_SETUP_DEVICE", "1") == "0" or device_count() < 1:
+        return None
+    t = i64(tets)
+    st = i64(surface_tris)
+    mk = np.ascontiguousarray(mask, dtype=np.uint8)
+    b = f64(bary)
+    ns = len(st)
+    elem = np.empty(max(ns * per_element, 1), dtype=np.int64)
+    w = np.empty((max(ns * per_element, 1), 4))
+    cnt = ctypes.c_int64(0)
+    rc = lib().spb_scatter_proxies(ptr(t), len(t), int(n), ptr(st), ns, ptr(mk), int(per_element), ptr(b), ptr(elem),
+                                   ptr(w), ctypes.byref(cnt))
+    if rc == SPB_ERR_ARG:
+        return None
+    check(rc)
+    k = int(cnt.value)
+    return elem[:k], w[:k]
 
 
 def posed(shape_id: int, rotation, translation) -> PosedCollider:
