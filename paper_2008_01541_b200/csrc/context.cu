@@ -1375,6 +1375,11 @@ static int frame_io_enqueue(Ctx* c, const double* att_targets, int32_t ncol, con
                             const spb_step_config* cfg, IoList& down, IoPending& pend) {
   if (ncol > spb::MAX_COLLIDERS) { spb::set_error("too many colliders"); return SPB_ERR_ARG; }
   SPB_CUDA(cudaStreamSynchronize(c->st));  // staging buffers are reused
+  // x first: its DMA (~60 us at cfg3) runs while the host packs the small block
+  const size_t xbytes = sizeof(double) * 3 * c->n;
+  IoList up;
+  up.add(c->x.p, x, xbytes);
+  TRY(io_upload(c, up, false));
   char* hs = c->io_small_host;
   if (c->na > 0 && att_targets) memcpy(hs + c->off_att, att_targets, sizeof(double) * 3 * c->na);
   c->cols_host->n = ncol;
@@ -1394,10 +1399,6 @@ static int frame_io_enqueue(Ctx* c, const double* att_targets, int32_t ncol, con
   TRY(c->sync_shapes());
   const size_t up_bytes = c->P ? c->off_tgt + sizeof(double) * 3 * c->P : c->off_act;
   SPB_CUDA(cudaMemcpyAsync(c->io_dev, hs, up_bytes, cudaMemcpyHostToDevice, c->st));
-  const size_t xbytes = sizeof(double) * 3 * c->n;
-  IoList up;
-  up.add(c->x.p, x, xbytes);
-  TRY(io_upload(c, up, false));
   TRY(frame_enqueue(c, cfg, nullptr, true));
   SPB_CUDA(cudaMemcpyAsync(hs + c->off_act, c->io_dev + c->off_act, c->off_end - c->off_act,
                            cudaMemcpyDeviceToHost, c->st));
