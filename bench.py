@@ -200,7 +200,7 @@ def cholesky_roofline(int8: bool, m: int, ms: float, fp64_equiv_tf: float, fp64_
     out["kernel"] = "k_cholesky_oz (INT8 tcgen05.mma, emulated-FP64 trailing updates; FP64 DMMA finalizes)"
     out["int8_tensor"] = {"achieved": tops, "peak": 2.0 * bf16, "unit": "TOPS (int8)", "frac": tops / (2.0 * bf16),
                           "peak_source": src, "int8_ops_per_launch": ops, "int8_ops_per_fp64_flop": ratio,
-                          "fp64_equivalent_ceiling_tflops": 2.0 * bf16 / ratio}
+                          "fp64_equivalent_ceiling_tflops": 2.0 * bf16 / ratio if ratio > 0 else None}
     return out
 
 
